@@ -1,0 +1,345 @@
+"""Model build on the B200: the drop-in for model_builder.compute_subgrid /
+build_model (/root/reference/pkg/src/flowmdp/model_builder.py:376-580).
+
+Host code here only marshals: it uploads the environment once
+(``DeviceEnv``), derives the per-action constants with the reference's
+Python-float arithmetic, allocates the device model and calls the C ABI.
+All per-(state, action, realization) work runs in ``k_build``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .core_types import (
+    OBJECTIVE_CODE,
+    CooBlock,
+    SparseModel,
+    SubGridSpec,
+    action_tables,
+)
+from .errors import ContractViolation
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# device-resident inputs
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DeviceEnv:
+    """Environment arrays resident in HBM (f64 / u8, reference layouts) plus
+    the per-layer obstacle summed-area tables used for box queries."""
+
+    grid: object
+    mean: object
+    modes: object
+    coeffs: object
+    g: object
+    mask: object
+    sat: object
+    n_modes: int
+    n_real: int
+    _vbound: dict = field(default_factory=dict)
+    _vmax: tuple | None = None
+
+    @classmethod
+    def from_host(cls, env, device=None, non_blocking: bool = False):
+        """Upload an Environment (reference or mirror types).  numpy arrays,
+        or (pinned) CPU torch tensors for non_blocking H2D."""
+        torch = _torch()
+        _lib.load()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+        def up(a, dtype):
+            t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+            return t.to(device=dev, dtype=dtype, non_blocking=non_blocking).contiguous()
+
+        grid, fld = env.grid, env.field
+        mask_src = env.obstacles.mask
+        if isinstance(mask_src, np.ndarray):
+            mask_src = mask_src.view(np.uint8) if mask_src.dtype == np.bool_ else mask_src.astype(np.uint8)
+        de = cls(
+            grid=grid,
+            mean=up(fld.mean, torch.float64),
+            modes=up(fld.modes, torch.float64),
+            coeffs=up(fld.coeffs, torch.float64),
+            g=up(env.scalar.g_mean, torch.float64),
+            mask=up(mask_src, torch.uint8),
+            sat=None,
+            n_modes=int(fld.modes.shape[0]),
+            n_real=int(fld.coeffs.shape[1]),
+        )
+        de._make_sat()
+        return de
+
+    def _make_sat(self):
+        torch = _torch()
+        g = self.grid
+        self.sat = torch.empty((g.nt, g.ny + 1, g.nx + 1), dtype=torch.int32, device=self.mean.device)
+        _lib.check(_lib.load().fm_mask_sat(self.mask.data_ptr(), g.nt, g.ny, g.nx, self.sat.data_ptr(),
+                                           _lib.stream_ptr()), "fm_mask_sat")
+
+    # -- C structs ---------------------------------------------------------
+    def fm_grid(self) -> _lib.FmGrid:
+        g = self.grid
+        return _lib.FmGrid(g.nx, g.ny, g.nt, float(g.dx), float(g.dt), float(g.origin[0]), float(g.origin[1]))
+
+    def fm_env(self) -> _lib.FmEnv:
+        return _lib.FmEnv(self.mean.data_ptr(), self.modes.data_ptr(), self.coeffs.data_ptr(),
+                          self.g.data_ptr(), self.mask.data_ptr(), self.n_modes, self.n_real)
+
+    # -- velocity statistics ------------------------------------------------
+    def velocity_max(self) -> tuple:
+        """Exact max |v_x|, |v_y| over (t, r, cell) -- compute_subgrid's scan."""
+        if self._vmax is None:
+            torch = _torch()
+            out = torch.zeros(2, dtype=torch.float64, device=self.mean.device)
+            _lib.check(_lib.load().fm_velocity_max(self.fm_grid(), self.fm_env(), out.data_ptr(),
+                                                   _lib.stream_ptr()), "fm_velocity_max")
+            h = out.cpu().numpy()
+            self._vmax = (float(h[0]), float(h[1]))
+        return self._vmax
+
+    def velocity_bound(self) -> tuple:
+        """Triangle bound of environment.py:404-419: device max-abs
+        reductions, then the reference's per-t combination on the host."""
+        if "b" not in self._vbound:
+            torch = _torch()
+            g, nm, nr = self.grid, self.n_modes, self.n_real
+            nc = g.nx * g.ny
+            L = _lib.load()
+            s = _lib.stream_ptr()
+            dev = self.mean.device
+            mean_mx = torch.empty(g.nt * 2, dtype=torch.float64, device=dev)
+            _lib.check(L.fm_maxabs_segments(self.mean.data_ptr(), g.nt * 2, nc, 2, 2, nc * 2, 1,
+                                            mean_mx.data_ptr(), s), "maxabs mean")
+            coef_mx = torch.zeros(max(g.nt * nm, 1), dtype=torch.float64, device=dev)
+            mode_mx = torch.zeros(max(nm * g.nt * 2, 1), dtype=torch.float64, device=dev)
+            if nm:
+                _lib.check(L.fm_maxabs_segments(self.coeffs.data_ptr(), g.nt * nm, nr, nm, nm, nr * nm, 1,
+                                                coef_mx.data_ptr(), s), "maxabs coeffs")
+                _lib.check(L.fm_maxabs_segments(self.modes.data_ptr(), nm * g.nt * 2, nc, 2, 2, nc * 2, 1,
+                                                mode_mx.data_ptr(), s), "maxabs modes")
+            mean_mx = mean_mx.cpu().numpy().reshape(g.nt, 2)
+            coef_mx = coef_mx.cpu().numpy()[: g.nt * nm].reshape(g.nt, nm)
+            mode_mx = mode_mx.cpu().numpy()[: nm * g.nt * 2].reshape(nm, g.nt, 2)
+            bounds = []
+            for c in (0, 1):
+                per_t = mean_mx[:, c].copy()
+                for m in range(nm):
+                    per_t = per_t + coef_mx[:, m] * mode_mx[m, :, c]
+                bounds.append(float(per_t.max()))
+            self._vbound["b"] = (bounds[0], bounds[1])
+        return self._vbound["b"]
+
+
+def gate_radius(denv: DeviceEnv, f_max: float) -> tuple:
+    """Obstacle-gate dilation radius in cells (model_builder.py:218-223)."""
+    bx, by = denv.velocity_bound()
+    g = denv.grid
+    rx = int(math.ceil((bx + f_max) * g.dt / g.dx)) + 1
+    ry = int(math.ceil((by + f_max) * g.dt / g.dx)) + 1
+    return rx, ry
+
+
+def subgrid_from_vmax(vmax: tuple, f_max: float, grid, buffer: int = 1) -> SubGridSpec:
+    """half_width = ceil((max|v_c| + f_max) * dt / dx) + buffer (model_builder.py:397-399)."""
+    if buffer < 1:
+        raise ContractViolation("buffer must be >= 1")
+    hx = int(math.ceil((vmax[0] + f_max) * grid.dt / grid.dx)) + buffer
+    hy = int(math.ceil((vmax[1] + f_max) * grid.dt / grid.dx)) + buffer
+    return SubGridSpec(half_width_x=hx, half_width_y=hy)
+
+
+def compute_subgrid(field, actions, grid, buffer: int = 1, device_env: DeviceEnv | None = None) -> SubGridSpec:
+    """Drop-in for model_builder.compute_subgrid (model_builder.py:376-399).
+
+    The exact max over every (t, realization, cell) runs in ``k_vmax``."""
+    if buffer < 1:
+        raise ContractViolation("buffer must be >= 1")
+    denv = device_env
+    if denv is None:
+        env = _FieldOnly(grid, field)
+        denv = DeviceEnv.from_host(env)
+    return subgrid_from_vmax(denv.velocity_max(), actions.f_max, grid, buffer)
+
+
+class _FieldOnly:
+    """Environment stand-in for compute_subgrid(field, ...) calls."""
+
+    def __init__(self, grid, field):
+        nt, ny, nx = field.mean.shape[:3]
+        self.grid = grid
+        self.field = field
+        self.scalar = type("S", (), {"g_mean": np.zeros((nt, ny, nx))})()
+        self.obstacles = type("O", (), {"mask": np.zeros((nt, ny, nx), dtype=bool)})()
+
+
+# ---------------------------------------------------------------------------
+# device model
+# ---------------------------------------------------------------------------
+
+def action_records(actions, rcfg, grid) -> np.ndarray:
+    """Per-action constants with the reference's rounding (model_builder.py:350-358)."""
+    vec, spd = action_tables(actions)
+    recs = np.zeros((vec.shape[0], 6), dtype=np.float64)
+    dt = float(grid.dt)
+    for a in range(vec.shape[0]):
+        f = float(spd[a])
+        neg_cff = -(rcfg.c_f * f * f)
+        if rcfg.objective == "time":
+            base = -dt
+        else:
+            base = -(rcfg.c_f * f * f) * dt
+        recs[a] = (vec[a, 0], vec[a, 1], base, base + rcfg.r_term, neg_cff, 0.0)
+    return recs
+
+
+@dataclass
+class DeviceModel:
+    """Compact model in HBM (see fm_model in include/flowmdp_b200.h)."""
+
+    grid: object
+    n_actions: int
+    n_real: int
+    subgrid: SubGridSpec
+    row_ptr: object      # int64  [n_rows]
+    row_nnz: object      # int16  [n_rows] (u16 bits)
+    reward: object       # f64    [n_rows]
+    entries: object      # int32  [capacity] (u32 bits)
+    d_nnz: object        # int64  [1]
+    nnz: int
+    t_range: tuple
+    j_range: tuple
+
+    @property
+    def n_rows(self) -> int:
+        return self.grid.nt * self.grid.nx * self.grid.ny * self.n_actions
+
+    @property
+    def nt(self) -> int:
+        return self.grid.nt
+
+    @property
+    def n_states(self) -> int:
+        return self.grid.nt * self.grid.nx * self.grid.ny + 1
+
+    def fm_model(self) -> _lib.FmModel:
+        g = self.grid
+        return _lib.FmModel(g.nx, g.ny, g.nt, self.n_actions, self.n_real,
+                            self.subgrid.half_width_x, self.subgrid.half_width_y,
+                            self.n_rows, self.row_ptr.data_ptr(), self.row_nnz.data_ptr(),
+                            self.reward.data_ptr(), self.entries.data_ptr(),
+                            int(self.entries.numel()), self.d_nnz.data_ptr())
+
+    def export_device(self):
+        """Canonical COO on the device: (block_off, rows, cols, vals, rewards)."""
+        torch = _torch()
+        dev = self.reward.device
+        nb = self.n_actions * self.grid.nt
+        scratch = torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev)
+        block_off = torch.zeros(nb + 1, dtype=torch.int64, device=dev)
+        rows = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+        cols = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(self.nnz, 1), dtype=torch.float64, device=dev)
+        rewards = torch.empty(self.n_rows, dtype=torch.float64, device=dev)
+        m = self.fm_model()
+        _lib.check(_lib.load().fm_export_coo(C.byref(m), scratch.data_ptr(), block_off.data_ptr(),
+                                             rows.data_ptr(), cols.data_ptr(), vals.data_ptr(),
+                                             rewards.data_ptr(), _lib.stream_ptr()), "fm_export_coo")
+        return block_off, rows[: self.nnz], cols[: self.nnz], vals[: self.nnz], rewards
+
+    def to_sparse_model(self) -> SparseModel:
+        """D2H into the reference's SparseModel (blocks[a][t] CooBlocks)."""
+        if self.t_range != (0, self.grid.nt) or self.j_range != (0, self.grid.ny):
+            raise ContractViolation("to_sparse_model needs a full (unsharded) model")
+        block_off, rows, cols, vals, rewards = self.export_device()
+        off = block_off.cpu().numpy()
+        rows_h = rows.cpu().numpy().view(np.uint32)
+        cols_h = cols.cpu().numpy().view(np.uint32)
+        vals_h = vals.cpu().numpy()
+        rew_h = rewards.cpu().numpy()
+        nt, na = self.grid.nt, self.n_actions
+        blocks = []
+        for a in range(na):
+            row = []
+            for t in range(nt):
+                lo, hi = int(off[a * nt + t]), int(off[a * nt + t + 1])
+                row.append(CooBlock(rows=rows_h[lo:hi], cols=cols_h[lo:hi], vals=vals_h[lo:hi], nnz=hi - lo))
+            blocks.append(row)
+        return SparseModel(blocks=blocks, rewards=rew_h, n_states=self.n_states, n_actions=na, nt=nt)
+
+
+def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridSpec,
+                       t_range: tuple | None = None, j_range: tuple | None = None,
+                       capacity_hint: int | None = None) -> DeviceModel:
+    """Run K_build over slabs t_range x row strip j_range; model stays in HBM."""
+    torch = _torch()
+    L = _lib.load()
+    grid = denv.grid
+    ti, tj = int(target[0]), int(target[1])
+    if not (0 <= ti < grid.nx and 0 <= tj < grid.ny):
+        raise ContractViolation(f"target cell {tuple(target)} outside grid")
+    t0, t1 = t_range if t_range is not None else (0, grid.nt)
+    j0, j1 = j_range if j_range is not None else (0, grid.ny)
+    dev = denv.mean.device
+    recs = action_records(actions, rcfg, grid)
+    na = recs.shape[0]
+    d_act = torch.from_numpy(recs).to(dev)
+    rx, ry = gate_radius(denv, float(actions.f_max))
+    hx, hy = subgrid.half_width_x, subgrid.half_width_y
+    nc = grid.nx * grid.ny
+    n_rows = grid.nt * nc * na
+    active_rows = (t1 - t0) * (j1 - j0) * grid.nx * na
+    n_slot1 = (2 * hx + 1) * (2 * hy + 1) + 1
+    cap = capacity_hint if capacity_hint else active_rows * min(n_slot1, denv.n_real, 6) + 1024
+
+    row_ptr = torch.empty(n_rows, dtype=torch.int64, device=dev)
+    row_nnz = torch.zeros(n_rows, dtype=torch.int16, device=dev)
+    reward = torch.zeros(n_rows, dtype=torch.float64, device=dev)
+    d_nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+    viol = torch.zeros(grid.nt * na, dtype=torch.int32, device=dev)
+    counter = torch.zeros(1, dtype=torch.int32, device=dev)
+    rw = _lib.FmReward(OBJECTIVE_CODE[rcfg.objective], float(rcfg.c_f), float(rcfg.c_r),
+                       float(rcfg.r_term), float(rcfg.r_outbound), ti, tj)
+    args = _lib.FmBuildArgs(denv.fm_grid(), denv.fm_env(), rw, d_act.data_ptr(), na, hx, hy, rx, ry,
+                            denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr())
+    for _attempt in range(2):
+        entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
+        dm = DeviceModel(grid=grid, n_actions=na, n_real=denv.n_real, subgrid=subgrid,
+                         row_ptr=row_ptr, row_nnz=row_nnz, reward=reward, entries=entries,
+                         d_nnz=d_nnz, nnz=0, t_range=(t0, t1), j_range=(j0, j1))
+        m = dm.fm_model()
+        needed = C.c_uint64(0)
+        vio = _lib.FmViolation()
+        st = L.fm_build(C.byref(args), C.byref(m), C.byref(needed), C.byref(vio), _lib.stream_ptr())
+        if st == _lib.FM_CAPACITY:
+            cap = int(needed.value) + 1024
+            d_nnz.zero_()
+            viol.zero_()
+            continue
+        _lib.check(st, "fm_build")
+        dm.nnz = int(needed.value)
+        return dm
+    raise RuntimeError("fm_build: capacity retry failed")
+
+
+def build_model(ctx, subgrid: SubGridSpec, n_threads: int = 1) -> SparseModel:
+    """Drop-in for model_builder.build_model (model_builder.py:532-580).
+
+    ``n_threads`` is accepted for signature compatibility; the GPU build is
+    deterministic and its output identical for any value."""
+    del n_threads
+    denv = ctx.device_env() if hasattr(ctx, "device_env") else DeviceEnv.from_host(ctx.env)
+    dm = build_device_model(denv, ctx.actions, ctx.rcfg, ctx.target, subgrid)
+    return dm.to_sparse_model()

@@ -1,0 +1,1199 @@
+// flowmdp_b200.cu -- B200 (sm_100a) kernels + C ABI for the planner hot path
+// of arXiv 2109.00857: ensemble-counted MDP model build and backward
+// Bellman solve.  See DESIGN.md for the data layout and roofline, and
+// include/flowmdp_b200.h for the reference function each entry replaces.
+//
+// Exactness contract: all position / reward / value
+// arithmetic is f64 with explicitly rounded __dadd_rn/__dmul_rn/__ddiv_rn
+// (and the file is compiled with -fmad=false), reproducing the numpy
+// reference's operation order so counts, columns, probabilities, rewards,
+// values and the policy are bit-identical.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+
+#include "../../include/flowmdp_b200.h"
+#include "fm_hypot.cuh"
+
+#define DADD(a, b) __dadd_rn((a), (b))
+#define DSUB(a, b) __dsub_rn((a), (b))
+#define DMUL(a, b) __dmul_rn((a), (b))
+#define DDIV(a, b) __ddiv_rn((a), (b))
+
+static constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int32_t fm_fail(int32_t code, const char *fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define FM_CK(expr)                                                                     \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fm_fail(FM_CUDA_ERROR, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define FM_CK_LAUNCH(name)                                                              \
+    do {                                                                                \
+        cudaError_t e_ = cudaGetLastError();                                            \
+        if (e_ != cudaSuccess)                                                          \
+            return fm_fail(FM_CUDA_ERROR, "launch %s: %s", name, cudaGetErrorString(e_)); \
+    } while (0)
+
+extern "C" int32_t fm_abi_version(void) { return 1; }
+extern "C" const char *fm_last_error(void) { return g_err.c_str(); }
+
+static int sm_count()
+{
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_max_f64(double v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+    return v;
+}
+
+// non-negative doubles order like their bit patterns
+__device__ __forceinline__ void atomic_max_nonneg(double *addr, double v)
+{
+    atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+// ---------------------------------------------------------------------------
+// K_vmax: compute_subgrid's exact scan (model_builder.py:392-396)
+// ---------------------------------------------------------------------------
+template <int NMX>
+__global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int rchunk, double *out2)
+{
+    const int nc = G.nx * G.ny;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y;
+    const int r_lo = blockIdx.z * rchunk;
+    const int r_hi = min(E.n_real, r_lo + rchunk);
+    double mx = 0.0, my = 0.0;
+    if (c < nc) {
+        const double2 mu = *reinterpret_cast<const double2 *>(E.mean + ((size_t)t * nc + c) * 2);
+        double2 md[NMX];
+#pragma unroll
+        for (int m = 0; m < NMX; ++m)
+            if (m < E.n_modes)
+                md[m] = *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + c) * 2);
+        for (int r = r_lo; r < r_hi; ++r) {
+            const double *cf = E.coeffs + ((size_t)t * E.n_real + r) * E.n_modes;
+            double vx = mu.x, vy = mu.y;
+#pragma unroll
+            for (int m = 0; m < NMX; ++m)
+                if (m < E.n_modes) {
+                    const double k = __ldg(cf + m);
+                    vx = DADD(vx, DMUL(k, md[m].x));
+                    vy = DADD(vy, DMUL(k, md[m].y));
+                }
+            mx = fmax(mx, fabs(vx));
+            my = fmax(my, fabs(vy));
+        }
+    }
+    mx = warp_max_f64(mx);
+    my = warp_max_f64(my);
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_nonneg(out2, mx);
+        atomic_max_nonneg(out2 + 1, my);
+    }
+}
+
+extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *stream)
+{
+    if (G.nx < 1 || G.ny < 1 || G.nt < 1 || E.n_real < 1 || E.n_modes < 0 || E.n_modes > 16)
+        return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims (n_modes must be <= 16)");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nc = G.nx * G.ny;
+    const int bx = (nc + 255) / 256;
+    // enough blocks to fill the machine several times over
+    long long base = (long long)bx * G.nt;
+    int rchunk = E.n_real;
+    long long want = 8LL * sm_count();
+    if (base < want) {
+        long long split = (want + base - 1) / base;
+        rchunk = (int)((E.n_real + split - 1) / split);
+        if (rchunk < 16) rchunk = 16;
+    }
+    dim3 grid(bx, G.nt, (E.n_real + rchunk - 1) / rchunk);
+    if (E.n_modes <= 4)
+        k_vmax<4><<<grid, 256, 0, s>>>(G, E, rchunk, d_out2);
+    else if (E.n_modes <= 8)
+        k_vmax<8><<<grid, 256, 0, s>>>(G, E, rchunk, d_out2);
+    else
+        k_vmax<16><<<grid, 256, 0, s>>>(G, E, rchunk, d_out2);
+    FM_CK_LAUNCH("k_vmax");
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// segmented max-abs (velocity_bound ingredients, environment.py:404-419)
+// ---------------------------------------------------------------------------
+__global__ void k_maxabs_seg(const double *src, int64_t seg_len, int64_t elem_stride, int64_t inner,
+                             int64_t outer_stride, int64_t inner_stride, double *out)
+{
+    const int64_t s = blockIdx.x;
+    const double *b = src + (s / inner) * outer_stride + (s % inner) * inner_stride;
+    double m = 0.0;
+    for (int64_t k = threadIdx.x; k < seg_len; k += blockDim.x) m = fmax(m, fabs(b[k * elem_stride]));
+    m = warp_max_f64(m);
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        m = warp_max_f64(m);
+        if (threadIdx.x == 0) out[s] = m;
+    }
+}
+
+extern "C" int32_t fm_maxabs_segments(const double *src, int64_t n_seg, int64_t seg_len, int64_t elem_stride,
+                                      int64_t inner, int64_t outer_stride, int64_t inner_stride,
+                                      double *d_out, void *stream)
+{
+    if (n_seg <= 0) return FM_OK;
+    if (inner < 1 || n_seg > 2147483647LL) return fm_fail(FM_BAD_ARG, "fm_maxabs_segments: bad shape");
+    k_maxabs_seg<<<(unsigned)n_seg, 256, 0, (cudaStream_t)stream>>>(src, seg_len, elem_stride, inner,
+                                                                      outer_stride, inner_stride, d_out);
+    FM_CK_LAUNCH("k_maxabs_seg");
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// obstacle-mask summed-area tables: sat[t][(j+1)*(nx+1) + (i+1)]
+// ---------------------------------------------------------------------------
+__global__ void k_mask_sat(const uint8_t *mask, int nt, int ny, int nx, int32_t *sat)
+{
+    const int t = blockIdx.x;
+    const uint8_t *m = mask + (size_t)t * nx * ny;
+    int32_t *S = sat + (size_t)t * (nx + 1) * (ny + 1);
+    const int W = nx + 1;
+    for (int i = threadIdx.x; i <= nx; i += blockDim.x) S[i] = 0;
+    for (int j = threadIdx.x; j < ny; j += blockDim.x) {
+        int32_t run = 0;
+        S[(j + 1) * W] = 0;
+        for (int i = 0; i < nx; ++i) {
+            run += m[j * nx + i] ? 1 : 0;
+            S[(j + 1) * W + i + 1] = run;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+        int32_t run = 0;
+        for (int j = 0; j < ny; ++j) {
+            run += S[(j + 1) * W + i + 1];
+            S[(j + 1) * W + i + 1] = run;
+        }
+    }
+}
+
+extern "C" int32_t fm_mask_sat(const uint8_t *mask, int32_t nt, int32_t ny, int32_t nx, int32_t *sat,
+                               void *stream)
+{
+    if (nt < 1 || ny < 1 || nx < 1) return fm_fail(FM_BAD_ARG, "fm_mask_sat: bad dims");
+    k_mask_sat<<<nt, 256, 0, (cudaStream_t)stream>>>(mask, nt, ny, nx, sat);
+    FM_CK_LAUNCH("k_mask_sat");
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K_build
+// ---------------------------------------------------------------------------
+enum : int { F_DT_ONE = 1, F_OX_ZERO = 2, F_DX_MUL = 4 };
+
+struct BuildK {
+    // grid
+    int nx, ny, nt, nc;
+    double dx, dt, ox, oy, inv_dx, half_dx;
+    // env
+    const double *mean, *modes, *coeffs, *g;
+    const uint8_t *mask;
+    const int32_t *sat;
+    int nm, nr;
+    // actions / rewards
+    const fm_action *act;
+    int na, obj;
+    double h_cr, r_term, r_out;
+    int tcell;
+    // sub-grid
+    int hx, hy, width, nslot, hw;
+    int rx, ry;
+    // task decomposition
+    int t0, t1, cell0, ncell;   // strip = cells [cell0, cell0 + ncell) of each layer
+    int CW, RW, AG, nag, groups;
+    long long n_tasks;
+    // outputs
+    uint64_t *row_ptr;
+    uint16_t *row_nnz;
+    double *reward;
+    uint32_t *entries;
+    unsigned long long capacity;
+    unsigned long long *nnz_counter;
+    uint32_t *viol;
+    unsigned int *task_counter;
+};
+
+// count of set mask cells at layer t inside [i0,i1] x [j0,j1] (clipped)
+__device__ __forceinline__ int box_count(const BuildK &K, int t, int i0, int i1, int j0, int j1)
+{
+    i0 = max(i0, 0);
+    j0 = max(j0, 0);
+    i1 = min(i1, K.nx - 1);
+    j1 = min(j1, K.ny - 1);
+    if (i0 > i1 || j0 > j1) return 0;
+    const int W = K.nx + 1;
+    const int32_t *S = K.sat + (size_t)t * W * (K.ny + 1);
+    return S[(j1 + 1) * W + i1 + 1] - S[j0 * W + i1 + 1] - S[(j1 + 1) * W + i0] + S[j0 * W + i0];
+}
+
+template <int FLAGS>
+__device__ __forceinline__ double to_cell(const BuildK &K, double x, double o)
+{
+    // (x - origin) / dx with the reference's rounding (model_builder.py:333-334)
+    double u = (FLAGS & F_OX_ZERO) ? x : DSUB(x, o);
+    return (FLAGS & F_DX_MUL) ? DMUL(u, K.inv_dx) : DDIV(u, K.dx);
+}
+
+// _segments_blocked for one segment (environment.py:338-368), preceded by
+// an exact-conservative bounding-box test against the mask SAT: samples are
+// monotone in frac, so every sample cell lies in the box spanned by p0 and
+// fl(p0 + delta); an empty box cannot block.
+template <int FLAGS>
+__device__ __forceinline__ bool seg_blocked(const BuildK &K, int t, double p0x, double p0y, double p1x, double p1y)
+{
+    const double ddx = DSUB(p1x, p0x), ddy = DSUB(p1y, p0y);
+    const double ex = DADD(p0x, ddx), ey = DADD(p0y, ddy);
+    const int ilo = __double2int_rd(to_cell<FLAGS>(K, fmin(p0x, ex), K.ox));
+    const int ihi = __double2int_rd(to_cell<FLAGS>(K, fmax(p0x, ex), K.ox));
+    const int jlo = __double2int_rd(to_cell<FLAGS>(K, fmin(p0y, ey), K.oy));
+    const int jhi = __double2int_rd(to_cell<FLAGS>(K, fmax(p0y, ey), K.oy));
+    if (box_count(K, t, ilo, ihi, jlo, jhi) == 0) return false;
+    const double len = fm_hypot(ddx, ddy);
+    double ns = ceil(DDIV(len, K.half_dx));
+    if (!(ns >= 1.0)) ns = 1.0;
+    const long long n = (long long)ns;
+    const uint8_t *mt = K.mask + (size_t)t * K.nc;
+    for (long long q = 0; q <= n; ++q) {
+        double frac = DDIV((double)q, ns);
+        if (frac > 1.0) frac = 1.0;
+        const double px = DADD(p0x, DMUL(frac, ddx));
+        const double py = DADD(p0y, DMUL(frac, ddy));
+        const long long i = __double2ll_rd(to_cell<FLAGS>(K, px, K.ox));
+        const long long j = __double2ll_rd(to_cell<FLAGS>(K, py, K.oy));
+        if (i >= 0 && i < K.nx && j >= 0 && j < K.ny && mt[j * K.nx + i]) return true;
+    }
+    return false;
+}
+
+// One warp = one task (t, group of CW source cells, group of <=32 actions).
+// Lane roles:
+//   row lane  (cs, a): owns the row (state t*N_c + c, action a); walks the
+//                      realizations in ascending order, so its reward sum is
+//                      the reference's sequential sum (model_builder.py:457);
+//                      its displacement histogram (u16 counters, two per
+//                      word, lane-interleaved -> conflict-free) lives in smem.
+//   recon lane (cs, rr): reconstructs v(t, c, r) for a chunk of RW
+//                      realizations into smem (environment.py:293-297), shared
+//                      by all AG row lanes of that cell.
+template <int NMX, int FLAGS>
+__global__ void __launch_bounds__(128) k_build(const BuildK K)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smem) + (size_t)warp * K.hw * 32;
+    double2 *vbuf = reinterpret_cast<double2 *>(smem + (size_t)nwarps * K.hw * 128) + warp * 32;
+
+    for (int w = 0; w < K.hw; ++w) hist[w * 32 + lane] = 0u;
+
+    const int cs_row = lane / K.AG, a_loc = lane - (lane / K.AG) * K.AG;
+    const bool row_lane = lane < K.CW * K.AG;
+    const int cs_rec = lane / K.RW, rr = lane - (lane / K.RW) * K.RW;
+    const bool rec_lane = lane < K.CW * K.RW;
+    const int nslot = K.nslot;
+
+    for (;;) {
+        unsigned task = 0;
+        if (lane == 0) task = atomicAdd(K.task_counter, 1u);
+        task = __shfl_sync(kFull, task, 0);
+        if ((long long)task >= K.n_tasks) break;
+        const int per_t = K.groups * K.nag;
+        const int t = K.t0 + (int)(task / per_t);
+        const int rem = (int)(task % per_t);
+        const int grp = rem / K.nag, ag = rem - (rem / K.nag) * K.nag;
+        const int a = ag * 32 + a_loc;
+        const int lc_row = grp * K.CW + cs_row;
+        const bool row_ok = row_lane && lc_row < K.ncell && a < K.na;
+        const int c = K.cell0 + lc_row;
+        const int ci = c % K.nx, cj = c / K.nx;
+        const bool horizon = (t + 1 >= K.nt);
+
+        // per-row constants
+        double x0 = 0, y0 = 0, ax = 0, ay = 0, base = 0, base_hit = 0, AB = 0;
+        bool terminal = false, obstacle = false, gate = false, landwin = false;
+        if (row_ok) {
+            x0 = DADD(K.ox, DMUL(DADD((double)ci, 0.5), K.dx));   // environment.py:99-100
+            y0 = DADD(K.oy, DMUL(DADD((double)cj, 0.5), K.dx));
+            const fm_action A = K.act[a];
+            ax = A.ax;
+            ay = A.ay;
+            base = A.base;
+            base_hit = A.base_hit;
+            terminal = (c == K.tcell);
+            obstacle = !terminal && K.mask[(size_t)t * K.nc + c];
+            if (!horizon) {
+                gate = box_count(K, t, ci - K.rx, ci + K.rx, cj - K.ry, cj + K.ry) > 0;
+                landwin = box_count(K, t + 1, ci - K.hx, ci + K.hx, cj - K.hy, cj + K.hy) > 0;
+                if (K.obj == FM_OBJ_NET_ENERGY)
+                    AB = DADD(A.neg_cff, DMUL(K.h_cr, K.g[(size_t)t * K.nc + c]));   // model_builder.py:358
+            }
+        }
+        const bool dead = terminal || obstacle;
+        const double dead_r = terminal ? 0.0 : K.r_out;
+        double S = 0.0;
+        bool viol = false;
+
+        if (horizon) {
+            // step_flat's horizon branch (model_builder.py:319-328): every
+            // realization -> SINK with r_outbound, then the dead override.
+            if (row_ok) {
+                const double rw = terminal ? 0.0 : K.r_out;
+                for (int r = 0; r < K.nr; ++r) S = DADD(S, rw);
+                hist[(nslot >> 1) * 32 + lane] = (uint32_t)K.nr << ((nslot & 1) << 4);
+            }
+        } else {
+            // recon-lane constants
+            const int lc_rec = grp * K.CW + cs_rec;
+            const bool rec_ok = rec_lane && lc_rec < K.ncell;
+            const int crec = K.cell0 + lc_rec;
+            double2 mu = make_double2(0.0, 0.0);
+            double2 md[NMX];
+            if (rec_ok) {
+                mu = *reinterpret_cast<const double2 *>(K.mean + ((size_t)t * K.nc + crec) * 2);
+#pragma unroll
+                for (int m = 0; m < NMX; ++m)
+                    if (m < K.nm)
+                        md[m] = *reinterpret_cast<const double2 *>(K.modes + (((size_t)m * K.nt + t) * K.nc + crec) * 2);
+            }
+            const double *cf_t = K.coeffs + (size_t)t * K.nr * K.nm;
+            const uint8_t *mask_n = K.mask + (size_t)(t + 1) * K.nc;
+            const double *g_n = K.g + (size_t)(t + 1) * K.nc;
+            const int vb = cs_row * K.RW;
+
+            for (int r0 = 0; r0 < K.nr; r0 += K.RW) {
+                const int r = r0 + rr;
+                if (rec_ok && r < K.nr) {
+                    const double *cf = cf_t + (size_t)r * K.nm;
+                    double vx = mu.x, vy = mu.y;
+#pragma unroll
+                    for (int m = 0; m < NMX; ++m)
+                        if (m < K.nm) {
+                            const double k = __ldg(cf + m);
+                            vx = DADD(vx, DMUL(k, md[m].x));
+                            vy = DADD(vy, DMUL(k, md[m].y));
+                        }
+                    vbuf[cs_rec * K.RW + rr] = make_double2(vx, vy);
+                }
+                __syncwarp();
+                const int nk = min(K.RW, K.nr - r0);
+                if (row_ok) {
+                    for (int k = 0; k < nk; ++k) {
+                        const double2 v = vbuf[vb + k];
+                        // x' = x0 + (v + a) * dt   (model_builder.py:332)
+                        double px = DADD(v.x, ax), py = DADD(v.y, ay);
+                        if (!(FLAGS & F_DT_ONE)) {
+                            px = DMUL(px, K.dt);
+                            py = DMUL(py, K.dt);
+                        }
+                        const double x1 = DADD(x0, px), y1 = DADD(y0, py);
+                        const int i1 = __double2int_rd(to_cell<FLAGS>(K, x1, K.ox));
+                        const int j1 = __double2int_rd(to_cell<FLAGS>(K, y1, K.oy));
+                        const int di = i1 - ci, dj = j1 - cj;
+                        const bool inb = (unsigned)i1 < (unsigned)K.nx && (unsigned)j1 < (unsigned)K.ny;
+                        const bool inwin = (unsigned)(di + K.hx) <= (unsigned)(2 * K.hx) &&
+                                           (unsigned)(dj + K.hy) <= (unsigned)(2 * K.hy);
+                        const int succ = j1 * K.nx + i1;
+                        bool bad = !inb;
+                        if (inb && (landwin || !inwin)) bad = mask_n[succ] != 0;        // landed in obstacle
+                        if (!bad && gate) bad = seg_blocked<FLAGS>(K, t, x0, y0, x1, y1);  // transit
+                        viol |= (!bad && !inwin);
+                        const bool hit = !bad && succ == K.tcell;
+                        double rw;
+                        if (K.obj == FM_OBJ_NET_ENERGY) {
+                            const double gd = inb ? __ldg(g_n + succ) : 0.0;
+                            const double b = DMUL(DADD(AB, DMUL(K.h_cr, gd)), K.dt);
+                            rw = hit ? DADD(b, K.r_term) : b;
+                        } else {
+                            rw = hit ? base_hit : base;
+                        }
+                        int slot = (dj + K.hy) * K.width + (di + K.hx);
+                        if (bad || !inwin) slot = nslot;
+                        if (bad) rw = K.r_out;
+                        if (dead) {
+                            slot = nslot;
+                            rw = dead_r;
+                        }
+                        S = DADD(S, rw);
+                        hist[(slot >> 1) * 32 + lane] += 1u << ((slot & 1) << 4);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+
+        if (__any_sync(kFull, viol) && viol && row_ok) atomicOr(K.viol + (size_t)t * K.na + a, 1u);
+
+        // ---- emit: nnz census, warp scan, bump allocation, slot-ordered fill
+        int nnz = 0;
+        if (row_ok)
+            for (int w = 0; w < K.hw; ++w) {
+                const uint32_t x = hist[w * 32 + lane];
+                nnz += ((x & 0xffffu) != 0) + ((x >> 16) != 0);
+            }
+        int incl = nnz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(kFull, incl, 31);
+        unsigned long long base_pos = 0;
+        if (lane == 0) base_pos = atomicAdd(K.nnz_counter, (unsigned long long)total);
+        base_pos = __shfl_sync(kFull, base_pos, 0);
+        if (row_ok) {
+            unsigned long long pos = base_pos + (unsigned long long)(incl - nnz);
+            const size_t row = ((size_t)t * K.nc + c) * K.na + a;
+            K.row_ptr[row] = pos;
+            K.row_nnz[row] = (uint16_t)nnz;
+            K.reward[row] = DDIV(S, (double)K.nr);   // finalize_rewards (model_builder.py:462-464)
+            for (int w = 0; w < K.hw; ++w) {
+                const uint32_t x = hist[w * 32 + lane];
+                if (!x) continue;
+                hist[w * 32 + lane] = 0u;
+                const uint32_t lo = x & 0xffffu, hi = x >> 16;
+                if (lo) {
+                    if (pos < K.capacity) K.entries[pos] = ((uint32_t)(2 * w) << 16) | lo;
+                    ++pos;
+                }
+                if (hi) {
+                    if (pos < K.capacity) K.entries[pos] = ((uint32_t)(2 * w + 1) << 16) | hi;
+                    ++pos;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Recomputes one (t, a) sweep over every (r, c) of the layer to reproduce
+// the reference's ContractViolation message (model_builder.py:430-438):
+// argmax over non-sink entries of |di|+|dj|, first flat index r*N_c + c.
+template <int FLAGS>
+__global__ void k_viol_report(const BuildK K, int t, int a, int pass, unsigned long long *best, int32_t *didj)
+{
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)K.nr * K.nc) return;
+    const int r = (int)(idx / K.nc), c = (int)(idx % K.nc);
+    const int ci = c % K.nx, cj = c / K.nx;
+    double vx = K.mean[((size_t)t * K.nc + c) * 2], vy = K.mean[((size_t)t * K.nc + c) * 2 + 1];
+    for (int m = 0; m < K.nm; ++m) {
+        const double k = K.coeffs[((size_t)t * K.nr + r) * K.nm + m];
+        const double *md = K.modes + (((size_t)m * K.nt + t) * K.nc + c) * 2;
+        vx = DADD(vx, DMUL(k, md[0]));
+        vy = DADD(vy, DMUL(k, md[1]));
+    }
+    const fm_action A = K.act[a];
+    const double x0 = DADD(K.ox, DMUL(DADD((double)ci, 0.5), K.dx));
+    const double y0 = DADD(K.oy, DMUL(DADD((double)cj, 0.5), K.dx));
+    double px = DADD(vx, A.ax), py = DADD(vy, A.ay);
+    px = DMUL(px, K.dt);
+    py = DMUL(py, K.dt);
+    const double x1 = DADD(x0, px), y1 = DADD(y0, py);
+    const int i1 = __double2int_rd(DDIV(DSUB(x1, K.ox), K.dx));
+    const int j1 = __double2int_rd(DDIV(DSUB(y1, K.oy), K.dx));
+    const bool inb = (unsigned)i1 < (unsigned)K.nx && (unsigned)j1 < (unsigned)K.ny;
+    bool bad = !inb;
+    if (inb) bad = K.mask[(size_t)(t + 1) * K.nc + j1 * K.nx + i1] != 0;
+    if (!bad && box_count(K, t, ci - K.rx, ci + K.rx, cj - K.ry, cj + K.ry) > 0)
+        bad = seg_blocked<0>(K, t, x0, y0, x1, y1);
+    if (bad) return;
+    const int di = i1 - ci, dj = j1 - cj;
+    const unsigned long long key = (unsigned long long)(abs(di) + abs(dj));
+    const unsigned long long packed = (key << 40) | (0xFFFFFFFFFFull - (unsigned long long)idx);
+    if (pass == 0) {
+        atomicMax(best, packed);
+    } else if (packed == *best) {
+        didj[0] = di;
+        didj[1] = dj;
+    }
+}
+
+static int32_t launch_build(const BuildK &K, int nm, int flags, size_t smem, int blocks, cudaStream_t s)
+{
+#define FM_BUILD_CASE(NMX, FL)                                                                 \
+    if (nmx == NMX && flags == FL) {                                                           \
+        auto kern = k_build<NMX, FL>;                                                          \
+        FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        int occ = 0;                                                                           \
+        FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));          \
+        if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", smem); \
+        int nb = blocks > 0 ? blocks : occ * sm_count();                                       \
+        kern<<<nb, 128, smem, s>>>(K);                                                         \
+        FM_CK_LAUNCH("k_build");                                                               \
+        return FM_OK;                                                                          \
+    }
+#define FM_BUILD_NM(NMX) \
+    FM_BUILD_CASE(NMX, 0) FM_BUILD_CASE(NMX, 1) FM_BUILD_CASE(NMX, 2) FM_BUILD_CASE(NMX, 3) \
+    FM_BUILD_CASE(NMX, 4) FM_BUILD_CASE(NMX, 5) FM_BUILD_CASE(NMX, 6) FM_BUILD_CASE(NMX, 7)
+    const int nmx = nm <= 4 ? 4 : (nm <= 8 ? 8 : 16);
+    FM_BUILD_NM(4)
+    FM_BUILD_NM(8)
+    FM_BUILD_NM(16)
+#undef FM_BUILD_NM
+#undef FM_BUILD_CASE
+    return fm_fail(FM_BAD_ARG, "k_build: unsupported n_modes %d", nm);
+}
+
+static bool is_pow2(double x)
+{
+    if (!(x > 0.0)) return false;
+    int e;
+    double m = frexp(x, &e);
+    return m == 0.5;
+}
+
+extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_needed, fm_violation *h_viol,
+                            void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    const fm_grid &G = h->grid;
+    if (G.nx < 1 || G.ny < 1 || G.nt < 1 || !(G.dx > 0) || !(G.dt > 0))
+        return fm_fail(FM_BAD_ARG, "fm_build: bad grid");
+    if (h->env.n_modes < 0 || h->env.n_modes > 16) return fm_fail(FM_BAD_ARG, "fm_build: n_modes must be in [0,16]");
+    if (h->env.n_real < 1 || h->env.n_real > 65535) return fm_fail(FM_BAD_ARG, "fm_build: n_real must be in [1,65535]");
+    if (h->n_actions < 1) return fm_fail(FM_BAD_ARG, "fm_build: need >= 1 action");
+    if (h->hx < 0 || h->hy < 0) return fm_fail(FM_BAD_ARG, "fm_build: negative sub-grid");
+    const long long nslot = (long long)(2 * h->hx + 1) * (2 * h->hy + 1);
+    if (nslot + 1 > 65535) return fm_fail(FM_BAD_ARG, "fm_build: sub-grid too large (%lld slots)", nslot);
+    if (h->t0 < 0 || h->t1 > G.nt || h->t0 >= h->t1 || h->j0 < 0 || h->j1 > G.ny || h->j0 >= h->j1)
+        return fm_fail(FM_BAD_ARG, "fm_build: bad slab/strip range");
+    if (M->n_actions != h->n_actions || M->nt != G.nt || M->nx != G.nx || M->ny != G.ny)
+        return fm_fail(FM_BAD_ARG, "fm_build: model header does not match the problem");
+
+    BuildK K;
+    K.nx = G.nx; K.ny = G.ny; K.nt = G.nt; K.nc = G.nx * G.ny;
+    K.dx = G.dx; K.dt = G.dt; K.ox = G.ox; K.oy = G.oy;
+    K.inv_dx = 1.0 / G.dx;
+    K.half_dx = 0.5 * G.dx;
+    K.mean = h->env.mean; K.modes = h->env.modes; K.coeffs = h->env.coeffs; K.g = h->env.g;
+    K.mask = h->env.mask; K.sat = h->mask_sat;
+    K.nm = h->env.n_modes; K.nr = h->env.n_real;
+    K.act = h->actions; K.na = h->n_actions; K.obj = h->reward.objective;
+    K.h_cr = 0.5 * h->reward.c_r;   // `0.5 * rcfg.c_r` (model_builder.py:358)
+    K.r_term = h->reward.r_term; K.r_out = h->reward.r_outbound;
+    if (h->reward.target_i < 0 || h->reward.target_i >= G.nx || h->reward.target_j < 0 || h->reward.target_j >= G.ny)
+        return fm_fail(FM_BAD_ARG, "target cell (%d, %d) outside grid", h->reward.target_i, h->reward.target_j);
+    K.tcell = h->reward.target_j * G.nx + h->reward.target_i;
+    K.hx = h->hx; K.hy = h->hy; K.width = 2 * h->hx + 1; K.nslot = (int)nslot;
+    K.hw = (int)((nslot + 2) / 2);
+    K.rx = h->rx; K.ry = h->ry;
+    K.t0 = h->t0; K.t1 = h->t1;
+    K.cell0 = h->j0 * G.nx; K.ncell = (h->j1 - h->j0) * G.nx;
+    K.AG = h->n_actions < 32 ? h->n_actions : 32;
+    K.nag = (h->n_actions + 31) / 32;
+    K.CW = 32 / K.AG; if (K.CW < 1) K.CW = 1;
+    K.RW = 32 / K.CW;
+    K.groups = (K.ncell + K.CW - 1) / K.CW;
+    K.n_tasks = (long long)(h->t1 - h->t0) * K.groups * K.nag;
+    if (K.n_tasks > 0xFFFFFFF0LL) return fm_fail(FM_BAD_ARG, "fm_build: too many tasks");
+    K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
+    K.entries = M->entries; K.capacity = M->capacity;
+    K.nnz_counter = reinterpret_cast<unsigned long long *>(M->d_nnz);
+    K.viol = h->viol_flags; K.task_counter = h->task_counter;
+
+    int flags = 0;
+    if (G.dt == 1.0) flags |= F_DT_ONE;
+    if (G.ox == 0.0 && G.oy == 0.0) flags |= F_OX_ZERO;
+    if (is_pow2(G.dx)) flags |= F_DX_MUL;
+
+    FM_CK(cudaMemsetAsync(h->task_counter, 0, sizeof(unsigned int), s));
+    const size_t smem = (size_t)4 * ((size_t)K.hw * 128 + 32 * sizeof(double2));
+    int32_t st = launch_build(K, K.nm, flags, smem, 0, s);
+    if (st != FM_OK) return st;
+
+    // census + violation flags back to the host (the reference raises
+    // before returning anything, so the error check is synchronous).
+    unsigned long long nnz = 0;
+    FM_CK(cudaMemcpyAsync(&nnz, M->d_nnz, sizeof(nnz), cudaMemcpyDeviceToHost, s));
+    std::vector<uint32_t> flags_h((size_t)G.nt * h->n_actions);
+    FM_CK(cudaMemcpyAsync(flags_h.data(), h->viol_flags, flags_h.size() * 4, cudaMemcpyDeviceToHost, s));
+    FM_CK(cudaStreamSynchronize(s));
+    for (int t = h->t0; t < h->t1; ++t)
+        for (int a = 0; a < h->n_actions; ++a) {
+            if (!flags_h[(size_t)t * h->n_actions + a]) continue;
+            // reproduce the reference message for the first (t, a)
+            unsigned long long *d_best;
+            int32_t *d_didj;
+            FM_CK(cudaMallocAsync(&d_best, sizeof(unsigned long long) + 2 * sizeof(int32_t), s));
+            d_didj = reinterpret_cast<int32_t *>(d_best + 1);
+            FM_CK(cudaMemsetAsync(d_best, 0, sizeof(unsigned long long) + 2 * sizeof(int32_t), s));
+            const long long n = (long long)K.nr * K.nc;
+            const unsigned nb = (unsigned)((n + 255) / 256);
+            k_viol_report<0><<<nb, 256, 0, s>>>(K, t, a, 0, d_best, d_didj);
+            k_viol_report<0><<<nb, 256, 0, s>>>(K, t, a, 1, d_best, d_didj);
+            FM_CK_LAUNCH("k_viol_report");
+            int32_t didj[2] = {0, 0};
+            FM_CK(cudaMemcpyAsync(didj, d_didj, sizeof(didj), cudaMemcpyDeviceToHost, s));
+            FM_CK(cudaFreeAsync(d_best, s));
+            FM_CK(cudaStreamSynchronize(s));
+            if (h_viol) {
+                h_viol->t = t; h_viol->a = a; h_viol->di = didj[0]; h_viol->dj = didj[1];
+            }
+            return fm_fail(FM_SUBGRID_OVERFLOW,
+                           "displacement (%d,%d) at t=%d, a=%d exceeds sub-grid half widths (%d,%d)",
+                           didj[0], didj[1], t, a, h->hx, h->hy);
+        }
+    if (h_needed) *h_needed = nnz;
+    if (nnz > M->capacity)
+        return fm_fail(FM_CAPACITY, "fm_build: entry capacity %llu < %llu needed",
+                       (unsigned long long)M->capacity, nnz);
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan (u64), three-phase, used by the exporters
+// ---------------------------------------------------------------------------
+static constexpr int kScanBlock = 1024;   // elements per block (256 thr x 4)
+
+__global__ void k_scan_block(uint64_t *data, int64_t n, uint64_t *block_sums)
+{
+    __shared__ uint64_t sh[256];
+    const int64_t base = (int64_t)blockIdx.x * kScanBlock;
+    uint64_t v[4];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = base + threadIdx.x * 4 + k;
+        v[k] = i < n ? data[i] : 0;
+        sum += v[k];
+    }
+    sh[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+        uint64_t y = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+        __syncthreads();
+        sh[threadIdx.x] += y;
+        __syncthreads();
+    }
+    uint64_t run = sh[threadIdx.x] - sum;   // exclusive prefix of this thread
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = base + threadIdx.x * 4 + k;
+        if (i < n) data[i] = run;
+        run += v[k];
+    }
+    if (threadIdx.x == 255 && block_sums) block_sums[blockIdx.x] = sh[255];
+}
+
+__global__ void k_scan_add(uint64_t *data, int64_t n, const uint64_t *block_offs)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) data[i] += block_offs[i / kScanBlock];
+}
+
+// in-place exclusive scan of data[0..n); returns through data; uses tmp
+static int32_t scan_u64(uint64_t *data, int64_t n, cudaStream_t s)
+{
+    if (n <= 0) return FM_OK;
+    const int64_t nb = (n + kScanBlock - 1) / kScanBlock;
+    if (nb == 1) {
+        k_scan_block<<<1, 256, 0, s>>>(data, n, nullptr);
+        FM_CK_LAUNCH("k_scan_block");
+        return FM_OK;
+    }
+    uint64_t *sums = nullptr;
+    FM_CK(cudaMallocAsync(&sums, (size_t)nb * sizeof(uint64_t), s));
+    k_scan_block<<<(unsigned)nb, 256, 0, s>>>(data, n, sums);
+    FM_CK_LAUNCH("k_scan_block");
+    int32_t st = scan_u64(sums, nb, s);
+    if (st != FM_OK) return st;
+    k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(data, n, sums);
+    FM_CK_LAUNCH("k_scan_add");
+    FM_CK(cudaFreeAsync(sums, s));
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// export to canonical COO blocks (model_builder.py:474-501, 568-573)
+// ---------------------------------------------------------------------------
+struct ModelK {
+    int nx, ny, nt, nc, na, nr, hx, hy, width, nslot;
+    long long n_rows, n_g;
+    const uint64_t *row_ptr;
+    const uint16_t *row_nnz;
+    const double *reward;
+    const uint32_t *entries;
+};
+
+static ModelK model_k(const fm_model *M)
+{
+    ModelK K;
+    K.nx = M->nx; K.ny = M->ny; K.nt = M->nt; K.nc = M->nx * M->ny; K.na = M->n_actions;
+    K.nr = M->n_real; K.hx = M->hx; K.hy = M->hy; K.width = 2 * M->hx + 1;
+    K.nslot = (2 * M->hx + 1) * (2 * M->hy + 1);
+    K.n_rows = M->n_rows; K.n_g = (long long)M->nt * K.nc;
+    K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward; K.entries = M->entries;
+    return K;
+}
+
+// counts in (a, t, c) order
+__global__ void k_export_count(const ModelK K, uint64_t *cnt)
+{
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= K.n_rows) return;
+    const long long c = idx % K.nc;
+    const long long at = idx / K.nc;
+    const long long t = at % K.nt, a = at / K.nt;
+    cnt[idx] = K.row_nnz[(t * K.nc + c) * K.na + a];
+}
+
+__global__ void k_export_fill(const ModelK K, const uint64_t *off, uint32_t *rows, uint32_t *cols, double *vals,
+                              double *rewards, uint64_t *block_off)
+{
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= K.n_rows) return;
+    const long long c = idx % K.nc;
+    const long long at = idx / K.nc;
+    const long long t = at % K.nt, a = at / K.nt;
+    const long long row = (t * K.nc + c) * K.na + a;
+    const long long s = t * K.nc + c;
+    rewards[a * K.n_g + s] = K.reward[row];
+    if (c == 0) block_off[at] = off[idx];
+    if (idx == K.n_rows - 1) block_off[(long long)K.na * K.nt] = off[idx] + K.row_nnz[row];
+    uint64_t pos = off[idx];
+    const uint64_t p = K.row_ptr[row];
+    const int n = K.row_nnz[row];
+    const int ci = (int)(c % K.nx), cj = (int)(c / K.nx);
+    for (int k = 0; k < n; ++k) {
+        const uint32_t e = K.entries[p + k];
+        const int slot = (int)(e >> 16);
+        const uint32_t count = e & 0xffffu;
+        uint32_t col;
+        if (slot == K.nslot) {
+            col = (uint32_t)K.n_g;
+        } else {
+            const int dj = slot / K.width - K.hy, di = slot % K.width - K.hx;
+            col = (uint32_t)((t + 1) * K.nc + (long long)(cj + dj) * K.nx + (ci + di));
+        }
+        rows[pos] = (uint32_t)s;
+        cols[pos] = col;
+        vals[pos] = DDIV((double)count, (double)K.nr);   // model_builder.py:491
+        ++pos;
+    }
+}
+
+extern "C" int32_t fm_export_coo(const fm_model *M, uint64_t *d_scratch, uint64_t *d_block_off, uint32_t *rows,
+                                 uint32_t *cols, double *vals, double *rewards, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    const ModelK K = model_k(M);
+    if (K.n_rows <= 0) return fm_fail(FM_BAD_ARG, "fm_export_coo: empty model");
+    const unsigned nb = (unsigned)((K.n_rows + 255) / 256);
+    k_export_count<<<nb, 256, 0, s>>>(K, d_scratch);
+    FM_CK_LAUNCH("k_export_count");
+    int32_t st = scan_u64(d_scratch, K.n_rows, s);
+    if (st != FM_OK) return st;
+    k_export_fill<<<nb, 256, 0, s>>>(K, d_scratch, rows, cols, vals, rewards, d_block_off);
+    FM_CK_LAUNCH("k_export_fill");
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K_solve: backward Bellman layer over the compact model
+// ---------------------------------------------------------------------------
+struct SolveK {
+    ModelK M;
+    int t, cell0, ncell;
+    int CW, AG, nag, groups;
+    const double *ptab;   // ptab[count] = count / n_real
+    double *V;
+    uint16_t *pi;
+};
+
+__global__ void k_prob_table(double *ptab, int nr)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k <= nr) ptab[k] = DDIV((double)k, (double)nr);
+}
+
+__global__ void __launch_bounds__(256) k_solve_layer(const SolveK S)
+{
+    extern __shared__ int soff[];   // slot -> dj*nx + di
+    const ModelK &K = S.M;
+    for (int k = threadIdx.x; k < K.nslot; k += blockDim.x)
+        soff[k] = (k / K.width - K.hy) * K.nx + (k % K.width - K.hx);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int grp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (grp >= S.groups) return;
+    const int cs = lane / S.AG, a_loc = lane - (lane / S.AG) * S.AG;
+    const int lc = grp * S.CW + cs;
+    const bool cell_ok = lane < S.CW * S.AG && lc < S.ncell;
+    const int c = S.cell0 + lc;
+    const int t = S.t;
+    const double *Vn = S.V + (size_t)(t + 1) * K.nc + c;   // only dereferenced for non-OUT slots
+    const double vsink = S.V[K.n_g];
+    double best = 0.0;
+    int best_a = -1;
+    for (int ag = 0; ag < S.nag; ++ag) {
+        const int a = ag * 32 + a_loc;
+        if (cell_ok && a < K.na) {
+            const size_t row = ((size_t)t * K.nc + c) * K.na + a;
+            const uint64_t p = K.row_ptr[row];
+            const int n = K.row_nnz[row];
+            double acc = 0.0;   // np.bincount starts every row at +0.0
+            for (int k = 0; k < n; ++k) {
+                const uint32_t e = __ldg(K.entries + p + k);
+                const int slot = (int)(e >> 16);
+                const double pr = __ldg(S.ptab + (e & 0xffffu));
+                const double vv = slot == K.nslot ? vsink : __ldg(Vn + soff[slot]);
+                acc = DADD(acc, DMUL(pr, vv));
+            }
+            const double q = DADD(K.reward[row], acc);   // q[a] = R + bincount (solver.py:69-71)
+            if (best_a < 0 || q > best) {
+                best = q;
+                best_a = a;
+            }
+        }
+    }
+    // first maximum across the AG lanes of this cell (np.argmax semantics)
+    for (int o = 1; o < 32; o <<= 1) {
+        const double ob = __shfl_down_sync(kFull, best, o);
+        const int oa = __shfl_down_sync(kFull, best_a, o);
+        const bool same_cell = (a_loc + o) < S.AG && lane + o < 32;
+        if (same_cell && oa >= 0 && (best_a < 0 || ob > best || (ob == best && oa < best_a))) {
+            best = ob;
+            best_a = oa;
+        }
+    }
+    if (cell_ok && a_loc == 0 && best_a >= 0) {
+        S.V[(size_t)t * K.nc + c] = best;
+        S.pi[(size_t)t * K.nc + c] = (uint16_t)best_a;
+    }
+}
+
+static int32_t solve_layer(const fm_model *M, const double *ptab, int t, int j0, int j1, double *V, uint16_t *pi,
+                           cudaStream_t s)
+{
+    SolveK S;
+    S.M = model_k(M);
+    S.t = t;
+    S.cell0 = j0 * M->nx;
+    S.ncell = (j1 - j0) * M->nx;
+    S.AG = M->n_actions < 32 ? M->n_actions : 32;
+    S.nag = (M->n_actions + 31) / 32;
+    S.CW = 32 / S.AG;
+    if (S.CW < 1) S.CW = 1;
+    S.groups = (S.ncell + S.CW - 1) / S.CW;
+    S.ptab = ptab;
+    S.V = V;
+    S.pi = pi;
+    const int wpb = 8;
+    const unsigned nb = (unsigned)((S.groups + wpb - 1) / wpb);
+    const size_t smem = sizeof(int) * (size_t)S.M.nslot;
+    k_solve_layer<<<nb, wpb * 32, smem, s>>>(S);
+    FM_CK_LAUNCH("k_solve_layer");
+    return FM_OK;
+}
+
+static double *prob_table(const fm_model *M, cudaStream_t s, int32_t *st)
+{
+    double *ptab = nullptr;
+    cudaError_t e = cudaMallocAsync(&ptab, sizeof(double) * (size_t)(M->n_real + 1), s);
+    if (e != cudaSuccess) {
+        *st = fm_fail(FM_CUDA_ERROR, "cudaMallocAsync: %s", cudaGetErrorString(e));
+        return nullptr;
+    }
+    k_prob_table<<<(M->n_real + 256) / 256, 256, 0, s>>>(ptab, M->n_real);
+    *st = FM_OK;
+    return ptab;
+}
+
+extern "C" int32_t fm_solve_backward(const fm_model *M, int32_t t_lo, int32_t t_hi, double *values,
+                                     uint16_t *policy, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    if (t_lo < 0 || t_hi > M->nt || t_lo >= t_hi) return fm_fail(FM_BAD_ARG, "fm_solve_backward: bad t range");
+    int32_t st;
+    double *ptab = prob_table(M, s, &st);
+    if (st != FM_OK) return st;
+    for (int t = t_hi - 1; t >= t_lo; --t) {
+        st = solve_layer(M, ptab, t, 0, M->ny, values, policy, s);
+        if (st != FM_OK) return st;
+    }
+    FM_CK(cudaFreeAsync(ptab, s));
+    return FM_OK;
+}
+
+extern "C" int32_t fm_solve_layer(const fm_model *M, int32_t t, int32_t j0, int32_t j1, double *values,
+                                  uint16_t *policy, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    if (t < 0 || t >= M->nt || j0 < 0 || j1 > M->ny || j0 >= j1)
+        return fm_fail(FM_BAD_ARG, "fm_solve_layer: bad range");
+    int32_t st;
+    double *ptab = prob_table(M, s, &st);
+    if (st != FM_OK) return st;
+    st = solve_layer(M, ptab, t, j0, j1, values, policy, s);
+    if (st != FM_OK) return st;
+    FM_CK(cudaFreeAsync(ptab, s));
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// general CSR path (host-supplied SparseModel): Jacobi VI, greedy, policy
+// ---------------------------------------------------------------------------
+__global__ void k_csr_count(const uint32_t *rows, const int64_t *seg_off, int na, int64_t n_g, uint64_t *cnt,
+                            int32_t *sorted)
+{
+    const int a = blockIdx.y;
+    const int64_t lo = seg_off[a], hi = seg_off[a + 1];
+    for (int64_t k = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < hi; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = rows[k];
+        if ((int64_t)r >= n_g) {
+            *sorted = 0;
+            continue;
+        }
+        atomicAdd(reinterpret_cast<unsigned long long *>(cnt + (int64_t)a * n_g + r), 1ull);
+        if (k > lo && rows[k - 1] > r) *sorted = 0;
+    }
+}
+
+extern "C" int32_t fm_csr_row_ptr(const uint32_t *rows, const int64_t *h_seg_off, int32_t na, int64_t n_g,
+                                  int64_t *row_ptr, int32_t *d_sorted_flag, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = (int64_t)na * n_g + 1;
+    FM_CK(cudaMemsetAsync(row_ptr, 0, sizeof(int64_t) * n, s));
+    int64_t *d_off = nullptr;
+    FM_CK(cudaMallocAsync(&d_off, sizeof(int64_t) * (na + 1), s));
+    FM_CK(cudaMemcpyAsync(d_off, h_seg_off, sizeof(int64_t) * (na + 1), cudaMemcpyHostToDevice, s));
+    const int one = 1;
+    FM_CK(cudaMemcpyAsync(d_sorted_flag, &one, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    dim3 grid(64, na);
+    k_csr_count<<<grid, 256, 0, s>>>(rows, d_off, na, n_g, reinterpret_cast<uint64_t *>(row_ptr), d_sorted_flag);
+    FM_CK_LAUNCH("k_csr_count");
+    int32_t st = scan_u64(reinterpret_cast<uint64_t *>(row_ptr), n, s);
+    if (st != FM_OK) return st;
+    FM_CK(cudaFreeAsync(d_off, s));
+    FM_CK(cudaStreamSynchronize(s));   // h_seg_off / `one` are host stack memory
+    return FM_OK;
+}
+
+struct CsrK {
+    int64_t n_g;
+    int na;
+    const int64_t *rp;
+    const uint32_t *cols;
+    const double *vals;
+    const double *R;
+};
+
+__device__ __forceinline__ double csr_q(const CsrK &C, int a, int64_t s, const double *v)
+{
+    const int64_t lo = C.rp[(int64_t)a * C.n_g + s], hi = C.rp[(int64_t)a * C.n_g + s + 1];
+    double acc = 0.0;
+    for (int64_t k = lo; k < hi; ++k) acc = DADD(acc, DMUL(C.vals[k], v[C.cols[k]]));
+    return DADD(C.R[(int64_t)a * C.n_g + s], acc);
+}
+
+// mode 0: v_out = max_a Q (Jacobi sweep); mode 1: fixed policy.
+// Residual = max |v_out - v_in| over all n_g + 1 entries; the last block
+// decides convergence (solver.py:95-99) so no host round trip is needed.
+struct JacK {
+    CsrK C;
+    const uint16_t *policy;
+    int mode;
+    double eps;
+    unsigned long long *res;       // [max_iter] residual bits
+    unsigned int *done_blocks;     // [max_iter]
+    int *done;                     // [1]
+    unsigned long long *stats;     // [2] iterations, residual bits
+};
+
+__global__ void __launch_bounds__(256) k_jacobi(const JacK J, int iter, const double *v_in, double *v_out)
+{
+    if (*((volatile int *)J.done)) return;
+    const CsrK &C = J.C;
+    double local = 0.0;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s <= C.n_g;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        double vn;
+        if (s == C.n_g) {
+            vn = 0.0;
+        } else if (J.mode == 0) {
+            vn = csr_q(C, 0, s, v_in);
+            for (int a = 1; a < C.na; ++a) {
+                const double q = csr_q(C, a, s, v_in);
+                if (q > vn) vn = q;
+            }
+        } else {
+            vn = csr_q(C, J.policy[s], s, v_in);
+        }
+        v_out[s] = vn;
+        const double d = fabs(DSUB(vn, v_in[s]));
+        local = (d > local || d != d) ? d : local;
+    }
+    // block max of non-negative (or NaN) bit patterns
+    unsigned long long b = (unsigned long long)__double_as_longlong(local);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(kFull, b, o);
+        b = y > b ? y : b;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(J.res + iter, b);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned ticket = atomicAdd(J.done_blocks + iter, 1u);
+        if (ticket == gridDim.x - 1) {
+            __threadfence();
+            const unsigned long long rb = atomicAdd(J.res + iter, 0ull);
+            const double r = __longlong_as_double((long long)rb);
+            J.stats[0] = (unsigned long long)(iter + 1);
+            J.stats[1] = rb;
+            if (r < J.eps) *J.done = 1;
+        }
+    }
+}
+
+static CsrK csr_k(const fm_csr *h)
+{
+    CsrK C;
+    C.n_g = h->n_g; C.na = h->n_actions; C.rp = h->row_ptr; C.cols = h->cols; C.vals = h->vals; C.R = h->rewards;
+    return C;
+}
+
+static int32_t run_jacobi(const fm_csr *h, const uint16_t *policy, int mode, double eps, int max_iter, double *v0,
+                          double *v1, uint64_t *d_stats, cudaStream_t s)
+{
+    if (max_iter < 1) return fm_fail(FM_BAD_ARG, "max_iterations must be >= 1");
+    JacK J;
+    J.C = csr_k(h);
+    J.policy = policy;
+    J.mode = mode;
+    J.eps = eps;
+    const size_t scratch = sizeof(unsigned long long) * max_iter + sizeof(unsigned int) * max_iter + sizeof(int) * 4;
+    unsigned char *buf = nullptr;
+    FM_CK(cudaMallocAsync(&buf, scratch, s));
+    FM_CK(cudaMemsetAsync(buf, 0, scratch, s));
+    J.res = reinterpret_cast<unsigned long long *>(buf);
+    J.done_blocks = reinterpret_cast<unsigned int *>(buf + sizeof(unsigned long long) * max_iter);
+    J.done = reinterpret_cast<int *>(buf + sizeof(unsigned long long) * max_iter + sizeof(unsigned int) * max_iter);
+    J.stats = reinterpret_cast<unsigned long long *>(d_stats);
+    FM_CK(cudaMemsetAsync(d_stats, 0, 2 * sizeof(uint64_t), s));
+    FM_CK(cudaMemsetAsync(v0, 0, sizeof(double) * (size_t)(h->n_g + 1), s));
+    const int64_t n = h->n_g + 1;
+    int nb = (int)((n + 255) / 256);
+    const int cap = 8 * sm_count();
+    if (nb > cap) nb = cap;
+    for (int it = 0; it < max_iter; ++it) {
+        const double *vin = (it & 1) ? v1 : v0;
+        double *vout = (it & 1) ? v0 : v1;
+        k_jacobi<<<nb, 256, 0, s>>>(J, it, vin, vout);
+    }
+    FM_CK_LAUNCH("k_jacobi");
+    FM_CK(cudaFreeAsync(buf, s));
+    return FM_OK;
+}
+
+extern "C" int32_t fm_jacobi(const fm_csr *h, double epsilon, int32_t max_iter, double *v0, double *v1,
+                             uint64_t *d_stats, void *stream)
+{
+    return run_jacobi(h, nullptr, 0, epsilon, max_iter, v0, v1, d_stats, (cudaStream_t)stream);
+}
+
+extern "C" int32_t fm_policy_value(const fm_csr *h, const uint16_t *policy, double epsilon, int32_t max_iter,
+                                   double *v0, double *v1, uint64_t *d_stats, void *stream)
+{
+    return run_jacobi(h, policy, 1, epsilon, max_iter, v0, v1, d_stats, (cudaStream_t)stream);
+}
+
+__global__ void k_greedy(const CsrK C, const double *v, uint16_t *act)
+{
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= C.n_g) return;
+    double best = csr_q(C, 0, s, v);
+    int ba = 0;
+    for (int a = 1; a < C.na; ++a) {
+        const double q = csr_q(C, a, s, v);
+        if (q > best) {
+            best = q;
+            ba = a;
+        }
+    }
+    act[s] = (uint16_t)ba;
+}
+
+extern "C" int32_t fm_greedy(const fm_csr *h, const double *values, uint16_t *actions, void *stream)
+{
+    const CsrK C = csr_k(h);
+    if (C.n_g <= 0) return FM_OK;
+    k_greedy<<<(unsigned)((C.n_g + 255) / 256), 256, 0, (cudaStream_t)stream>>>(C, values, actions);
+    FM_CK_LAUNCH("k_greedy");
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// FP64 pipe probe (roofline denominator)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fp64_probe(double *sink, int iters)
+{
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+    const double m = 0.999999999, b = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = DADD(DMUL(x[k], m), b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 12345.678) sink[0] = s;
+}
+
+extern "C" int32_t fm_fp64_probe(double *d_sink, int32_t blocks, int32_t iters, void *stream)
+{
+    k_fp64_probe<<<blocks, 256, 0, (cudaStream_t)stream>>>(d_sink, iters);
+    FM_CK_LAUNCH("k_fp64_probe");
+    return FM_OK;
+}

@@ -1,0 +1,45 @@
+"""End-to-end planner: sub-grid sizing -> model build -> backward solve, all
+in HBM.  This is the path BASELINE.json's metric times:
+the reference's compute_subgrid + build_model + value_iteration
+(pipeline.py:96-136) without the file round trips.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .builder import DeviceEnv, build_device_model, subgrid_from_vmax
+from .core_types import PolicyValue, SubGridSpec
+from .solver import solve_backward
+
+
+@dataclass
+class Plan:
+    subgrid: SubGridSpec
+    model: object        # builder.DeviceModel
+    values: object       # torch f64 [N_g + 1] (device)
+    policy: object       # torch int16 (u16 bits) [N_g] (device)
+
+    def policy_value(self) -> PolicyValue:
+        """Host copy in the reference's PolicyValue shape.  The backward sweep
+        is exact in one pass; iterations_run reports the pass count (nt) --
+        use solver.value_iteration for the reference's Jacobi sweep count."""
+        v = self.values.cpu().numpy()
+        a = self.policy.cpu().numpy().view(np.uint16).copy()
+        return PolicyValue(values=v, actions=a, iterations_run=self.model.grid.nt, residual=0.0,
+                           converged=True)
+
+
+def plan(env, actions, rcfg, target, buffer: int = 1, device_env: DeviceEnv | None = None,
+         subgrid: SubGridSpec | None = None) -> Plan:
+    """Size the sub-grid (k_vmax), build the model (k_build) and solve it
+    backward in time (k_solve_layer).  Inputs already resident in HBM are
+    reused through ``device_env``."""
+    denv = device_env if device_env is not None else DeviceEnv.from_host(env)
+    sub = subgrid if subgrid is not None else subgrid_from_vmax(denv.velocity_max(), actions.f_max,
+                                                               denv.grid, buffer)
+    dm = build_device_model(denv, actions, rcfg, target, sub)
+    values, policy = solve_backward(dm)
+    return Plan(subgrid=sub, model=dm, values=values, policy=policy)

@@ -1,0 +1,239 @@
+"""CUDA path vs the CPU oracle, bit for bit, through the drop-in API.
+
+Every comparison is exact (digests over dtype+shape+bytes): transition
+counts, CSR indices, probabilities, rewards, values (sign bits included)
+and the policy.  The oracle itself is pinned to the reference by
+tests/test_oracle_golden.py; where the input digest matches the golden
+record, results are also checked against the reference's own digests."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import RANDOM_SEEDS, make_named_env, make_random_env, make_tiny_env, make_zero_flow_env
+from golden_util import env_digest, model_digest, sha
+
+pytestmark = pytest.mark.gpu
+
+fm = pytest.importorskip("paper_2109_00857_b200")
+from paper_2109_00857_b200 import (  # noqa: E402
+    ActionSpace,
+    ContractViolation,
+    RewardConfig,
+    SolverConfig,
+    StepContext,
+    SubGridSpec,
+)
+from paper_2109_00857_b200.builder import DeviceEnv, build_device_model  # noqa: E402
+from paper_2109_00857_b200.solver import solve_backward  # noqa: E402
+
+
+def _gpu_case(env, acts, rcfg, target, rec=None):
+    """Build + solve on the GPU and on the oracle; assert exact equality."""
+    ctx = StepContext(env, acts, rcfg, target)
+    sub = fm.compute_subgrid(env.field, acts, env.grid)
+    hx, hy = O.compute_subgrid(env.field, acts.f_max, env.grid)
+    assert (sub.half_width_x, sub.half_width_y) == (hx, hy)
+    gm = fm.build_model(ctx, sub)
+    om = O.build_model(env, acts, rcfg, target, hx, hy, n_threads=os.cpu_count() or 1)
+    assert gm.nnz_total() == om.nnz_total()
+    for a in range(acts.n_actions):
+        for t in range(env.grid.nt):
+            g, (r, c, v) = gm.blocks[a][t], om.blocks[a][t]
+            assert np.array_equal(g.rows, r) and np.array_equal(g.cols, c), (a, t)
+            assert sha(g.vals) == sha(v), (a, t)
+    assert sha(gm.rewards) == sha(om.rewards)
+    assert model_digest(gm) == model_digest(om)
+
+    # drop-in Jacobi value iteration (exact reference semantics)
+    pv = fm.value_iteration(gm)
+    ov, oa, oit, ores, oconv = O.value_iteration(om)
+    assert sha(pv.values) == sha(ov) and sha(pv.actions) == sha(oa)
+    assert (pv.iterations_run, pv.residual, pv.converged) == (oit, ores, oconv)
+
+    # planner path: device model + backward sweep
+    denv = ctx.device_env()
+    dm = build_device_model(denv, acts, rcfg, target, sub)
+    vals, pol = solve_backward(dm)
+    if ores == 0.0:
+        assert sha(vals.cpu().numpy()) == sha(ov)
+        assert sha(pol.cpu().numpy().view(np.uint16)) == sha(oa)
+
+    # extract_policy / policy_value drop-ins
+    assert np.array_equal(fm.extract_policy(gm, ov), O.extract_policy(om, ov))
+    assert sha(fm.policy_value(gm, oa)) == sha(O.policy_value(om, oa))
+
+    if rec is not None and env_digest(env) == rec["input_sha"]:
+        assert model_digest(gm) == rec["model_sha"]
+        assert sha(pv.values) == rec["solve"]["values_sha"]
+        assert sha(pv.actions) == rec["solve"]["actions_sha"]
+    return gm, om, pv
+
+
+@pytest.mark.parametrize("seed", RANDOM_SEEDS)
+def test_random_env_parity(golden, seed):
+    env, acts, rcfg, target = make_random_env(seed)
+    gm, om, _ = _gpu_case(env, acts, rcfg, target, golden["random"][str(seed)])
+    for mi in (1, 2, 3):
+        pv = fm.value_iteration(gm, SolverConfig(max_iterations=mi))
+        v, a, it, res, conv = O.value_iteration(om, max_iterations=mi)
+        assert sha(pv.values) == sha(v) and sha(pv.actions) == sha(a)
+        assert (pv.iterations_run, pv.residual, pv.converged) == (it, res, conv)
+
+
+@pytest.mark.parametrize("objective", ["time", "energy", "net_energy"])
+def test_tiny_env_parity(golden, objective):
+    acts = ActionSpace(n_headings=8, n_speeds=2, f_max=1.0)
+    rcfg = RewardConfig(objective=objective, c_f=1.0, c_r=0.8, r_term=50.0, r_outbound=-200.0)
+    _gpu_case(make_tiny_env(), acts, rcfg, (4, 4), golden["tiny"][objective])
+
+
+def test_hand_chain():
+    env = make_zero_flow_env(nx=3, ny=1, nt=4, dt=1.0)
+    acts = ActionSpace(n_headings=1, n_speeds=1, f_max=1.0)
+    rcfg = RewardConfig(objective="time", r_term=10.0, r_outbound=-50.0)
+    _, _, pv = _gpu_case(env, acts, rcfg, (2, 0))
+    assert pv.values[0] == 8.0 and pv.values[1] == 9.0 and pv.values[env.grid.sink] == 0.0
+
+
+def test_subgrid_violation_message(golden):
+    from paper_2109_00857_b200 import DOVelocityField, Environment, GridSpec, ObstacleMask, ScalarMeanField
+    grid = GridSpec(nx=8, ny=4, nt=3, dx=1.0, dt=1.0)
+    mean = np.zeros((3, 4, 8, 2))
+    mean[..., 0] = 2.0
+    env = Environment(grid=grid, field=DOVelocityField(mean, np.zeros((0, 3, 4, 8, 2)), np.zeros((3, 3, 0))),
+                      scalar=ScalarMeanField(np.ones((3, 4, 8))),
+                      obstacles=ObstacleMask(np.zeros((3, 4, 8), dtype=bool)))
+    ctx = StepContext(env, ActionSpace(4, 1, 0.5), RewardConfig("time", r_term=10.0, r_outbound=-100.0), (7, 3))
+    with pytest.raises(ContractViolation) as ei:
+        fm.build_model(ctx, SubGridSpec(1, 1))
+    assert str(ei.value) == golden["violation_message"]
+
+
+def test_buffer_guard():
+    env = make_zero_flow_env()
+    with pytest.raises(ContractViolation):
+        fm.compute_subgrid(env.field, ActionSpace(4, 1, 1.0), env.grid, buffer=0)
+
+
+@pytest.mark.parametrize("objective", ["time", "energy", "net_energy"])
+def test_smoke_parity(golden, objective):
+    env, acts, _, target, start = make_named_env("smoke")
+    rcfg = RewardConfig(objective, c_f=1.0, c_r=0.5, r_term=100.0, r_outbound=-300.0)
+    rec = golden["named"][f"smoke_{objective}"]
+    _, _, pv = _gpu_case(env, acts, rcfg, target, rec)
+    assert pv.values[env.grid.state_index(*start, 0)] == rec["v_start"]
+
+
+@pytest.mark.parametrize("objective", ["time", "energy", "net_energy"])
+def test_desk_parity(golden, objective):
+    env, acts, _, target, start = make_named_env("desk")
+    rcfg = RewardConfig(objective, c_f=1.0, c_r=0.5, r_term=100.0, r_outbound=-300.0)
+    rec = golden["named"][f"desk_{objective}"]
+    _, _, pv = _gpu_case(env, acts, rcfg, target, rec)
+    if env_digest(env) == rec["input_sha"]:
+        assert pv.values[env.grid.state_index(*start, 0)] == rec["v_start"]
+        assert pv.iterations_run == rec["solve"]["iterations_run"]
+
+
+def test_strip_and_slab_sharding_union_equals_full():
+    """Spatial strips x time slabs built separately produce the same rows."""
+    env, acts, rcfg, target, _ = make_named_env("smoke")
+    denv = DeviceEnv.from_host(env)
+    sub = fm.compute_subgrid(env.field, acts, env.grid, device_env=denv)
+    full = build_device_model(denv, acts, rcfg, target, sub)
+    full_vals, full_pol = solve_backward(full)
+    ny, nt = env.grid.ny, env.grid.nt
+    import torch
+    nnz = torch.zeros_like(full.row_nnz)
+    rew = torch.zeros_like(full.reward)
+    for j0, j1 in ((0, 3), (3, 7), (7, ny)):
+        for t0, t1 in ((0, 4), (4, nt)):
+            part = build_device_model(denv, acts, rcfg, target, sub, t_range=(t0, t1), j_range=(j0, j1))
+            nc, na = env.grid.nx * ny, acts.n_actions
+            rows = torch.arange(full.n_rows, device=part.reward.device)
+            t_of = rows // (nc * na)
+            j_of = (rows // na) % nc // env.grid.nx
+            sel = (t_of >= t0) & (t_of < t1) & (j_of >= j0) & (j_of < j1)
+            nnz[sel] = part.row_nnz[sel]
+            rew[sel] = part.reward[sel]
+            # entries of every selected row match the full build's
+            p_idx = part.row_ptr[sel].cpu().numpy()
+            f_idx = full.row_ptr[sel].cpu().numpy()
+            n = part.row_nnz[sel].cpu().numpy()
+            pe = part.entries.cpu().numpy()
+            fe = full.entries.cpu().numpy()
+            for a, b, k in zip(p_idx, f_idx, n):
+                assert np.array_equal(pe[a:a + k], fe[b:b + k])
+    assert torch.equal(nnz, full.row_nnz) and torch.equal(rew, full.reward)
+
+
+def test_paper_scale_slabs_vs_oracle():
+    """C2 geometry (100x100, 16 actions) with 1000 realizations: every slab
+    on the GPU, three slabs (first, middle, horizon) on the oracle."""
+    from paper_2109_00857_b200 import workloads
+    w = workloads.get("paper").with_(grid=workloads.GridSpec(nx=100, ny=100, nt=100, dx=1.0, dt=1.0),
+                                     n_realizations=1000)
+    env = w.environment()
+    acts, rcfg, target = w.actions(), w.reward_config(), w.target
+    ctx = StepContext(env, acts, rcfg, target)
+    sub = fm.compute_subgrid(env.field, acts, env.grid)
+    assert (sub.half_width_x, sub.half_width_y) == O.compute_subgrid(env.field, acts.f_max, env.grid)
+    gm = fm.build_model(ctx, sub)
+    slabs = (0, 44, 99)
+    for t in slabs:
+        om = O.build_model(env, acts, rcfg, target, sub.half_width_x, sub.half_width_y,
+                           n_threads=os.cpu_count() or 1, t_range=(t, t + 1))
+        for a in range(acts.n_actions):
+            g = gm.blocks[a][t]
+            r, c, v = om.blocks[a][t]
+            assert np.array_equal(g.rows, r) and np.array_equal(g.cols, c) and sha(g.vals) == sha(v), (t, a)
+        n_g = env.grid.n_states
+        nc = env.grid.n_cells
+        gr = gm.rewards.reshape(acts.n_actions, n_g)[:, t * nc:(t + 1) * nc]
+        orr = om.rewards.reshape(acts.n_actions, n_g)[:, t * nc:(t + 1) * nc]
+        assert sha(gr) == sha(orr)
+    # size-independent properties over the whole model
+    n_r = env.field.n_realizations
+    for a in range(acts.n_actions):
+        for t in range(env.grid.nt):
+            b = gm.blocks[a][t]
+            counts = np.rint(b.vals * n_r)
+            per_row = np.bincount(b.rows.astype(np.int64) - t * env.grid.n_cells, weights=counts,
+                                  minlength=env.grid.n_cells)
+            assert (per_row == n_r).all()
+            same = np.diff(b.rows.astype(np.int64)) == 0
+            assert (np.diff(b.rows.astype(np.int64)) >= 0).all()
+            assert (np.diff(b.cols.astype(np.int64))[same] > 0).all()
+    # backward sweep == exact Jacobi on the full model
+    pv = fm.value_iteration(gm)
+    vals, pol = solve_backward(build_device_model(ctx.device_env(), acts, rcfg, target, sub))
+    assert pv.residual == 0.0
+    assert sha(vals.cpu().numpy()) == sha(pv.values)
+    assert sha(pol.cpu().numpy().view(np.uint16)) == sha(pv.actions)
+
+
+def test_reference_types_accepted():
+    """Objects from another package with the reference's attribute names work."""
+    env, acts, rcfg, target = make_random_env(7003)
+
+    class Acts:
+        n_headings, n_speeds, f_max = acts.n_headings, acts.n_speeds, acts.f_max
+
+        def vectors(self):
+            return acts.vectors()
+
+        def speeds(self):
+            return acts.speeds()
+
+        n_actions = acts.n_actions
+
+    ctx = StepContext(env, Acts(), rcfg, target)
+    sub = fm.compute_subgrid(env.field, Acts(), env.grid)
+    m = fm.build_model(ctx, sub)
+    om = O.build_model(env, acts, rcfg, target, sub.half_width_x, sub.half_width_y)
+    assert model_digest(m) == model_digest(om)
