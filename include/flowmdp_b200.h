@@ -120,6 +120,8 @@ typedef struct {
 /* ---- version / errors -------------------------------------------------- */
 int32_t fm_abi_version(void);
 const char *fm_last_error(void);
+/* Number of kernels this library has launched in the process so far. */
+int64_t fm_kernel_launches(void);
 
 /* ---- sub-grid sizing ---------------------------------------------------- */
 /* compute_subgrid's exact scan, model_builder.py:392-396: d_out2 receives

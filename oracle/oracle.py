@@ -51,6 +51,7 @@ class _Problem(C.Structure):
         ("target_i", C.c_int32), ("target_j", C.c_int32),
         ("hx", C.c_int32), ("hy", C.c_int32),
         ("rx", C.c_int32), ("ry", C.c_int32),
+        ("j0", C.c_int32), ("j1", C.c_int32),
     ]
 
 
@@ -166,7 +167,7 @@ def _problem(env, actions, rcfg, target, hx=0, hy=0):
         vec.shape[0], vec.ctypes.data, spd.ctypes.data,
         OBJECTIVE_CODE[rcfg.objective], float(rcfg.c_f), float(rcfg.c_r),
         float(rcfg.r_term), float(rcfg.r_outbound),
-        int(target[0]), int(target[1]), int(hx), int(hy), rx, ry,
+        int(target[0]), int(target[1]), int(hx), int(hy), rx, ry, 0, 0,
     )
     return P, keep
 
@@ -193,9 +194,13 @@ def compute_subgrid(field, f_max: float, grid, buffer: int = 1) -> tuple[int, in
 
 
 def build_model(env, actions, rcfg, target, hx, hy, n_threads: int = 1,
-                t_range: tuple[int, int] | None = None) -> OracleModel:
-    """model_builder.py:532-580.  Raises OracleViolation on sub-grid overflow."""
+                t_range: tuple[int, int] | None = None,
+                j_range: tuple[int, int] | None = None) -> OracleModel:
+    """model_builder.py:532-580.  Raises OracleViolation on sub-grid overflow.
+    t_range / j_range restrict the build to slabs / source-row strips."""
     P, keep = _problem(env, actions, rcfg, target, hx, hy)
+    if j_range is not None:
+        P.j0, P.j1 = int(j_range[0]), int(j_range[1])
     L = lib()
     nt = env.grid.nt
     t0, t1 = t_range if t_range is not None else (0, nt)

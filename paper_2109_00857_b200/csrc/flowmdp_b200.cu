@@ -12,6 +12,7 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -48,8 +49,20 @@ static int32_t fm_fail(int32_t code, const char *fmt, ...)
             return fm_fail(FM_CUDA_ERROR, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
     } while (0)
 
+static std::atomic<long long> g_launches{0};
+
+// every kernel launch site reports through here (fm_kernel_launches)
+#define FM_CK_LAUNCH_N(name, n)                                                         \
+    do {                                                                                \
+        g_launches += (n);                                                              \
+        cudaError_t e_ = cudaGetLastError();                                            \
+        if (e_ != cudaSuccess)                                                          \
+            return fm_fail(FM_CUDA_ERROR, "launch %s: %s", name, cudaGetErrorString(e_)); \
+    } while (0)
+
 #define FM_CK_LAUNCH(name)                                                              \
     do {                                                                                \
+        g_launches += 1;                                                                \
         cudaError_t e_ = cudaGetLastError();                                            \
         if (e_ != cudaSuccess)                                                          \
             return fm_fail(FM_CUDA_ERROR, "launch %s: %s", name, cudaGetErrorString(e_)); \
@@ -57,6 +70,7 @@ static int32_t fm_fail(int32_t code, const char *fmt, ...)
 
 extern "C" int32_t fm_abi_version(void) { return 1; }
 extern "C" const char *fm_last_error(void) { return g_err.c_str(); }
+extern "C" int64_t fm_kernel_launches(void) { return g_launches.load(); }
 
 static int sm_count()
 {
@@ -669,7 +683,7 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
             const unsigned nb = (unsigned)((n + 255) / 256);
             k_viol_report<0><<<nb, 256, 0, s>>>(K, t, a, 0, d_best, d_didj);
             k_viol_report<0><<<nb, 256, 0, s>>>(K, t, a, 1, d_best, d_didj);
-            FM_CK_LAUNCH("k_viol_report");
+            FM_CK_LAUNCH_N("k_viol_report", 2);
             int32_t didj[2] = {0, 0};
             FM_CK(cudaMemcpyAsync(didj, d_didj, sizeof(didj), cudaMemcpyDeviceToHost, s));
             FM_CK(cudaFreeAsync(d_best, s));
@@ -943,7 +957,9 @@ static double *prob_table(const fm_model *M, cudaStream_t s, int32_t *st)
         return nullptr;
     }
     k_prob_table<<<(M->n_real + 256) / 256, 256, 0, s>>>(ptab, M->n_real);
-    *st = FM_OK;
+    g_launches += 1;
+    e = cudaGetLastError();
+    *st = e == cudaSuccess ? FM_OK : fm_fail(FM_CUDA_ERROR, "launch k_prob_table: %s", cudaGetErrorString(e));
     return ptab;
 }
 
@@ -1130,7 +1146,7 @@ static int32_t run_jacobi(const fm_csr *h, const uint16_t *policy, int mode, dou
         double *vout = (it & 1) ? v0 : v1;
         k_jacobi<<<nb, 256, 0, s>>>(J, it, vin, vout);
     }
-    FM_CK_LAUNCH("k_jacobi");
+    FM_CK_LAUNCH_N("k_jacobi", max_iter);
     FM_CK(cudaFreeAsync(buf, s));
     return FM_OK;
 }

@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "flowmdp_b200.h")
 
 def _declared_functions():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int32_t|const char \*)\s*(fm_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int32_t|int64_t|const char \*)\s*(fm_\w+)\s*\(", src, flags=re.M)))
 
 
 def test_header_declares_abi():
