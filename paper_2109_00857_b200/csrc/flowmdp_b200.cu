@@ -241,7 +241,8 @@ extern "C" int32_t fm_mask_sat(const uint8_t *mask, int32_t nt, int32_t ny, int3
 // ---------------------------------------------------------------------------
 // K_build
 // ---------------------------------------------------------------------------
-enum : int { F_DT_ONE = 1, F_OX_ZERO = 2, F_DX_MUL = 4 };
+enum : int { F_DT_ONE = 1, F_OX_ZERO = 2, F_DX_MUL = 4, F_DX_ONE = 8, F_NET = 16 };
+enum : int { RF_DEAD = 1, RF_TERMINAL = 2, RF_GATE = 4, RF_LANDWIN = 8 };
 
 struct BuildK {
     // grid
@@ -264,6 +265,8 @@ struct BuildK {
     int t0, t1, cell0, ncell;   // strip = cells [cell0, cell0 + ncell) of each layer
     int CW, RW, AG, nag, groups;
     long long n_tasks;
+    // per-warp shared-memory carve-up (bytes)
+    int smem_warp, off_vbuf, off_coef, off_modes;
     // outputs
     uint64_t *row_ptr;
     uint16_t *row_nnz;
@@ -288,12 +291,14 @@ __device__ __forceinline__ int box_count(const BuildK &K, int t, int i0, int i1,
     return S[(j1 + 1) * W + i1 + 1] - S[j0 * W + i1 + 1] - S[(j1 + 1) * W + i0] + S[j0 * W + i0];
 }
 
+// (x - origin) / dx with the reference's rounding (model_builder.py:333-334);
+// the flags drop operations that are exact identities for this grid.
 template <int FLAGS>
-__device__ __forceinline__ double to_cell(const BuildK &K, double x, double o)
+__device__ __forceinline__ double to_cell(double x, double o, double dx, double inv_dx)
 {
-    // (x - origin) / dx with the reference's rounding (model_builder.py:333-334)
-    double u = (FLAGS & F_OX_ZERO) ? x : DSUB(x, o);
-    return (FLAGS & F_DX_MUL) ? DMUL(u, K.inv_dx) : DDIV(u, K.dx);
+    const double u = (FLAGS & F_OX_ZERO) ? x : DSUB(x, o);
+    if (FLAGS & F_DX_ONE) return u;
+    return (FLAGS & F_DX_MUL) ? DMUL(u, inv_dx) : DDIV(u, dx);
 }
 
 // _segments_blocked for one segment (environment.py:338-368), preceded by
@@ -305,10 +310,10 @@ __device__ __forceinline__ bool seg_blocked(const BuildK &K, int t, double p0x, 
 {
     const double ddx = DSUB(p1x, p0x), ddy = DSUB(p1y, p0y);
     const double ex = DADD(p0x, ddx), ey = DADD(p0y, ddy);
-    const int ilo = __double2int_rd(to_cell<FLAGS>(K, fmin(p0x, ex), K.ox));
-    const int ihi = __double2int_rd(to_cell<FLAGS>(K, fmax(p0x, ex), K.ox));
-    const int jlo = __double2int_rd(to_cell<FLAGS>(K, fmin(p0y, ey), K.oy));
-    const int jhi = __double2int_rd(to_cell<FLAGS>(K, fmax(p0y, ey), K.oy));
+    const int ilo = __double2int_rd(to_cell<FLAGS>(fmin(p0x, ex), K.ox, K.dx, K.inv_dx));
+    const int ihi = __double2int_rd(to_cell<FLAGS>(fmax(p0x, ex), K.ox, K.dx, K.inv_dx));
+    const int jlo = __double2int_rd(to_cell<FLAGS>(fmin(p0y, ey), K.oy, K.dx, K.inv_dx));
+    const int jhi = __double2int_rd(to_cell<FLAGS>(fmax(p0y, ey), K.oy, K.dx, K.inv_dx));
     if (box_count(K, t, ilo, ihi, jlo, jhi) == 0) return false;
     const double len = fm_hypot(ddx, ddy);
     double ns = ceil(DDIV(len, K.half_dx));
@@ -320,12 +325,63 @@ __device__ __forceinline__ bool seg_blocked(const BuildK &K, int t, double p0x, 
         if (frac > 1.0) frac = 1.0;
         const double px = DADD(p0x, DMUL(frac, ddx));
         const double py = DADD(p0y, DMUL(frac, ddy));
-        const long long i = __double2ll_rd(to_cell<FLAGS>(K, px, K.ox));
-        const long long j = __double2ll_rd(to_cell<FLAGS>(K, py, K.oy));
+        const long long i = __double2ll_rd(to_cell<FLAGS>(px, K.ox, K.dx, K.inv_dx));
+        const long long j = __double2ll_rd(to_cell<FLAGS>(py, K.oy, K.dx, K.inv_dx));
         if (i >= 0 && i < K.nx && j >= 0 && j < K.ny && mt[j * K.nx + i]) return true;
     }
     return false;
 }
+
+struct SlowOut {
+    double rw;
+    int slot;
+    int viol;
+};
+
+// Every transition the fast path cannot prove ordinary: landing outside the
+// row's clipped window (domain exit or sub-grid overflow), rows near an
+// obstacle (landing / transit tests), dead source cells.  Reads its
+// parameters from a global copy of BuildK so the call does not force the
+// kernel-parameter block onto the stack.
+template <int FLAGS>
+__device__ __noinline__ SlowOut slow_step(const BuildK *__restrict__ Kg, int t, int ci, int cj, double x0, double y0,
+                                          double x1, double y1, int i1, int j1, int rflags, double AB, double base,
+                                          double base_hit)
+{
+    const BuildK &K = *Kg;
+    const int di = i1 - ci, dj = j1 - cj;
+    const bool inb = (unsigned)i1 < (unsigned)K.nx && (unsigned)j1 < (unsigned)K.ny;
+    const bool inwin = (unsigned)(di + K.hx) <= (unsigned)(2 * K.hx) && (unsigned)(dj + K.hy) <= (unsigned)(2 * K.hy);
+    const int succ = j1 * K.nx + i1;
+    bool bad = !inb;
+    if (inb && ((rflags & RF_LANDWIN) || !inwin)) bad = K.mask[(size_t)(t + 1) * K.nc + succ] != 0;  // landed
+    if (!bad && (rflags & RF_GATE)) bad = seg_blocked<FLAGS>(K, t, x0, y0, x1, y1);                    // transit
+    SlowOut o;
+    o.viol = (!bad && !inwin);
+    const bool hit = !bad && succ == K.tcell;
+    if (K.obj == FM_OBJ_NET_ENERGY) {
+        const double gd = inb ? K.g[(size_t)(t + 1) * K.nc + succ] : 0.0;
+        const double b = DMUL(DADD(AB, DMUL(K.h_cr, gd)), K.dt);
+        o.rw = hit ? DADD(b, K.r_term) : b;
+    } else {
+        o.rw = hit ? base_hit : base;
+    }
+    o.slot = (bad || !inwin) ? K.nslot : (dj + K.hy) * K.width + (di + K.hx);
+    if (bad) o.rw = K.r_out;
+    if (rflags & RF_DEAD) {   // after the overflow check (model_builder.py:445-452)
+        o.slot = K.nslot;
+        o.rw = (rflags & RF_TERMINAL) ? 0.0 : K.r_out;
+    }
+    return o;
+}
+
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 // One warp = one task (t, group of CW source cells, group of <=32 actions).
 // Lane roles:
@@ -336,23 +392,29 @@ __device__ __forceinline__ bool seg_blocked(const BuildK &K, int t, double p0x, 
 //                      word, lane-interleaved -> conflict-free) lives in smem.
 //   recon lane (cs, rr): reconstructs v(t, c, r) for a chunk of RW
 //                      realizations into smem (environment.py:293-297), shared
-//                      by all AG row lanes of that cell.
-template <int NMX, int FLAGS>
-__global__ void __launch_bounds__(128) k_build(const BuildK K)
+//                      by all AG row lanes of that cell.  Coefficients of the
+//                      next chunk stream in with cp.async while the row lanes
+//                      work on the current one.
+template <int FLAGS>
+__global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *__restrict__ Kg)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
-    uint32_t *hist = reinterpret_cast<uint32_t *>(smem) + (size_t)warp * K.hw * 32;
-    double2 *vbuf = reinterpret_cast<double2 *>(smem + (size_t)nwarps * K.hw * 128) + warp * 32;
+    unsigned char *wbase = smem + (size_t)warp * K.smem_warp;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(wbase);
+    double2 *vbuf = reinterpret_cast<double2 *>(wbase + K.off_vbuf);
+    double *coef = reinterpret_cast<double *>(wbase + K.off_coef);     // [2][RW * nm]
+    double2 *modes_s = reinterpret_cast<double2 *>(wbase + K.off_modes);  // [CW][nm]
 
     for (int w = 0; w < K.hw; ++w) hist[w * 32 + lane] = 0u;
 
-    const int cs_row = lane / K.AG, a_loc = lane - (lane / K.AG) * K.AG;
-    const bool row_lane = lane < K.CW * K.AG;
-    const int cs_rec = lane / K.RW, rr = lane - (lane / K.RW) * K.RW;
-    const bool rec_lane = lane < K.CW * K.RW;
-    const int nslot = K.nslot;
+    const int AG = K.AG, RW = K.RW, CW = K.CW, nm = K.nm, nr = K.nr;
+    const int cs_row = lane / AG, a_loc = lane - cs_row * AG;
+    const bool row_lane = lane < CW * AG;
+    const int cs_rec = lane / RW, rr = lane - cs_rec * RW;
+    const bool rec_lane = lane < CW * RW;
+    const int nslot = K.nslot, W = K.width;
+    const int coef_stride = RW * nm;
 
     for (;;) {
         unsigned task = 0;
@@ -364,15 +426,16 @@ __global__ void __launch_bounds__(128) k_build(const BuildK K)
         const int rem = (int)(task % per_t);
         const int grp = rem / K.nag, ag = rem - (rem / K.nag) * K.nag;
         const int a = ag * 32 + a_loc;
-        const int lc_row = grp * K.CW + cs_row;
+        const int lc_row = grp * CW + cs_row;
         const bool row_ok = row_lane && lc_row < K.ncell && a < K.na;
         const int c = K.cell0 + lc_row;
         const int ci = c % K.nx, cj = c / K.nx;
         const bool horizon = (t + 1 >= K.nt);
 
-        // per-row constants
+        // ---- per-row constants
         double x0 = 0, y0 = 0, ax = 0, ay = 0, base = 0, base_hit = 0, AB = 0;
-        bool terminal = false, obstacle = false, gate = false, landwin = false;
+        int rflags = RF_DEAD, ilc = 0, jlc = 0, wi = -1, wj = -1, soff = 0, tslot = -1;
+        bool terminal = false;
         if (row_ok) {
             x0 = DADD(K.ox, DMUL(DADD((double)ci, 0.5), K.dx));   // environment.py:99-100
             y0 = DADD(K.oy, DMUL(DADD((double)cj, 0.5), K.dx));
@@ -382,105 +445,155 @@ __global__ void __launch_bounds__(128) k_build(const BuildK K)
             base = A.base;
             base_hit = A.base_hit;
             terminal = (c == K.tcell);
-            obstacle = !terminal && K.mask[(size_t)t * K.nc + c];
+            const bool obstacle = !terminal && K.mask[(size_t)t * K.nc + c];
+            rflags = (terminal || obstacle) ? RF_DEAD : 0;
+            if (terminal) rflags |= RF_TERMINAL;
             if (!horizon) {
-                gate = box_count(K, t, ci - K.rx, ci + K.rx, cj - K.ry, cj + K.ry) > 0;
-                landwin = box_count(K, t + 1, ci - K.hx, ci + K.hx, cj - K.hy, cj + K.hy) > 0;
+                if (box_count(K, t, ci - K.rx, ci + K.rx, cj - K.ry, cj + K.ry) > 0) rflags |= RF_GATE;
+                if (box_count(K, t + 1, ci - K.hx, ci + K.hx, cj - K.hy, cj + K.hy) > 0) rflags |= RF_LANDWIN;
                 if (K.obj == FM_OBJ_NET_ENERGY)
                     AB = DADD(A.neg_cff, DMUL(K.h_cr, K.g[(size_t)t * K.nc + c]));   // model_builder.py:358
             }
+            // window [ci-hx, ci+hx] x [cj-hy, cj+hy] clipped to the grid: a
+            // landing inside it is in-domain and inside the sub-grid
+            ilc = max(ci - K.hx, 0);
+            jlc = max(cj - K.hy, 0);
+            wi = min(ci + K.hx, K.nx - 1) - ilc;
+            wj = min(cj + K.hy, K.ny - 1) - jlc;
+            soff = -((cj - K.hy) * W + (ci - K.hx));    // slot = j1*W + i1 + soff
+            const int tci = K.tcell % K.nx, tcj = K.tcell / K.nx;
+            if ((unsigned)(tci - ilc) <= (unsigned)wi && (unsigned)(tcj - jlc) <= (unsigned)wj)
+                tslot = tcj * W + tci + soff;
         }
-        const bool dead = terminal || obstacle;
-        const double dead_r = terminal ? 0.0 : K.r_out;
+        const bool row_clear = row_ok && rflags == 0;
         double S = 0.0;
-        bool viol = false;
+        int viol = 0;
 
         if (horizon) {
             // step_flat's horizon branch (model_builder.py:319-328): every
             // realization -> SINK with r_outbound, then the dead override.
             if (row_ok) {
                 const double rw = terminal ? 0.0 : K.r_out;
-                for (int r = 0; r < K.nr; ++r) S = DADD(S, rw);
-                hist[(nslot >> 1) * 32 + lane] = (uint32_t)K.nr << ((nslot & 1) << 4);
+                for (int r = 0; r < nr; ++r) S = DADD(S, rw);
+                hist[(nslot >> 1) * 32 + lane] = (uint32_t)nr << ((nslot & 1) << 4);
             }
         } else {
-            // recon-lane constants
-            const int lc_rec = grp * K.CW + cs_rec;
-            const bool rec_ok = rec_lane && lc_rec < K.ncell;
-            const int crec = K.cell0 + lc_rec;
-            double2 mu = make_double2(0.0, 0.0);
-            double2 md[NMX];
-            if (rec_ok) {
-                mu = *reinterpret_cast<const double2 *>(K.mean + ((size_t)t * K.nc + crec) * 2);
-#pragma unroll
-                for (int m = 0; m < NMX; ++m)
-                    if (m < K.nm)
-                        md[m] = *reinterpret_cast<const double2 *>(K.modes + (((size_t)m * K.nt + t) * K.nc + crec) * 2);
+            // stage the CW cells' modes, issue chunk 0's coefficients
+            for (int i = lane; i < CW * nm; i += 32) {
+                const int cs = i / nm, m = i - (i / nm) * nm;
+                const int lc = grp * CW + cs;
+                if (lc < K.ncell)
+                    modes_s[i] = *reinterpret_cast<const double2 *>(
+                        K.modes + (((size_t)m * K.nt + t) * K.nc + K.cell0 + lc) * 2);
             }
-            const double *cf_t = K.coeffs + (size_t)t * K.nr * K.nm;
-            const uint8_t *mask_n = K.mask + (size_t)(t + 1) * K.nc;
+            const int lc_rec = grp * CW + cs_rec;
+            const bool rec_ok = rec_lane && lc_rec < K.ncell;
+            double2 mu = make_double2(0.0, 0.0);
+            if (rec_ok) mu = *reinterpret_cast<const double2 *>(K.mean + ((size_t)t * K.nc + K.cell0 + lc_rec) * 2);
+            const double *cf_t = K.coeffs + (size_t)t * nr * nm;
+            {
+                const int n_el = min(RW, nr) * nm;
+                for (int i = lane; i < n_el; i += 32) cp_async8(coef + i, cf_t + i);
+            }
+            cp_async_commit();
             const double *g_n = K.g + (size_t)(t + 1) * K.nc;
-            const int vb = cs_row * K.RW;
+            const int vb = cs_row * RW;
+            const double dt = K.dt, ox = K.ox, oy = K.oy, dx = K.dx, inv_dx = K.inv_dx;
+            const double h_cr = K.h_cr, r_term = K.r_term;
+            const int nx = K.nx;
+            int buf = 0;
 
-            for (int r0 = 0; r0 < K.nr; r0 += K.RW) {
+#define FM_STEP(V, SLOT, RWV)                                                                          \
+    {                                                                                                  \
+        double px_ = DADD((V).x, ax), py_ = DADD((V).y, ay);                                           \
+        if (!(FLAGS & F_DT_ONE)) {                                                                     \
+            px_ = DMUL(px_, dt);                                                                       \
+            py_ = DMUL(py_, dt);                                                                       \
+        }                                                                                              \
+        const double x1_ = DADD(x0, px_), y1_ = DADD(y0, py_);                                         \
+        const int i1_ = __double2int_rd(to_cell<FLAGS>(x1_, ox, dx, inv_dx));                          \
+        const int j1_ = __double2int_rd(to_cell<FLAGS>(y1_, oy, dx, inv_dx));                          \
+        if (row_clear && (unsigned)(i1_ - ilc) <= (unsigned)wi && (unsigned)(j1_ - jlc) <= (unsigned)wj) { \
+            SLOT = j1_ * W + i1_ + soff;                                                               \
+            const bool hit_ = SLOT == tslot;                                                           \
+            if (FLAGS & F_NET) {                                                                       \
+                const double gd_ = __ldg(g_n + j1_ * nx + i1_);                                        \
+                double b_ = DADD(AB, DMUL(h_cr, gd_));                                                 \
+                if (!(FLAGS & F_DT_ONE)) b_ = DMUL(b_, dt);                                            \
+                RWV = hit_ ? DADD(b_, r_term) : b_;                                                    \
+            } else {                                                                                   \
+                RWV = hit_ ? base_hit : base;                                                          \
+            }                                                                                          \
+        } else {                                                                                       \
+            const SlowOut o_ = slow_step<FLAGS>(Kg, t, ci, cj, x0, y0, x1_, y1_, i1_, j1_, rflags, AB, \
+                                                base, base_hit);                                       \
+            SLOT = o_.slot;                                                                            \
+            RWV = o_.rw;                                                                               \
+            viol |= o_.viol;                                                                           \
+        }                                                                                              \
+    }
+#define FM_HIST(SLOT) hist[((SLOT) >> 1) * 32 + lane] += 1u << (((SLOT) & 1) << 4)
+
+            for (int r0 = 0; r0 < nr; r0 += RW) {
+                // prefetch the next chunk's coefficients into the other buffer
+                if (r0 + RW < nr) {
+                    const int n_el = min(RW, nr - r0 - RW) * nm;
+                    const double *src = cf_t + (size_t)(r0 + RW) * nm;
+                    double *dst = coef + (buf ^ 1) * coef_stride;
+                    for (int i = lane; i < n_el; i += 32) cp_async8(dst + i, src + i);
+                }
+                cp_async_commit();
+                cp_async_wait1();
+                __syncwarp();
                 const int r = r0 + rr;
-                if (rec_ok && r < K.nr) {
-                    const double *cf = cf_t + (size_t)r * K.nm;
+                if (rec_ok && r < nr) {
+                    const double *cf = coef + buf * coef_stride + rr * nm;
+                    const double2 *md = modes_s + cs_rec * nm;
                     double vx = mu.x, vy = mu.y;
-#pragma unroll
-                    for (int m = 0; m < NMX; ++m)
-                        if (m < K.nm) {
-                            const double k = __ldg(cf + m);
-                            vx = DADD(vx, DMUL(k, md[m].x));
-                            vy = DADD(vy, DMUL(k, md[m].y));
-                        }
-                    vbuf[cs_rec * K.RW + rr] = make_double2(vx, vy);
+                    for (int m = 0; m < nm; ++m) {
+                        const double k = cf[m];
+                        const double2 mm = md[m];
+                        vx = DADD(vx, DMUL(k, mm.x));
+                        vy = DADD(vy, DMUL(k, mm.y));
+                    }
+                    vbuf[cs_rec * RW + rr] = make_double2(vx, vy);
                 }
                 __syncwarp();
-                const int nk = min(K.RW, K.nr - r0);
+                const int nk = min(RW, nr - r0);
                 if (row_ok) {
-                    for (int k = 0; k < nk; ++k) {
-                        const double2 v = vbuf[vb + k];
-                        // x' = x0 + (v + a) * dt   (model_builder.py:332)
-                        double px = DADD(v.x, ax), py = DADD(v.y, ay);
-                        if (!(FLAGS & F_DT_ONE)) {
-                            px = DMUL(px, K.dt);
-                            py = DMUL(py, K.dt);
-                        }
-                        const double x1 = DADD(x0, px), y1 = DADD(y0, py);
-                        const int i1 = __double2int_rd(to_cell<FLAGS>(K, x1, K.ox));
-                        const int j1 = __double2int_rd(to_cell<FLAGS>(K, y1, K.oy));
-                        const int di = i1 - ci, dj = j1 - cj;
-                        const bool inb = (unsigned)i1 < (unsigned)K.nx && (unsigned)j1 < (unsigned)K.ny;
-                        const bool inwin = (unsigned)(di + K.hx) <= (unsigned)(2 * K.hx) &&
-                                           (unsigned)(dj + K.hy) <= (unsigned)(2 * K.hy);
-                        const int succ = j1 * K.nx + i1;
-                        bool bad = !inb;
-                        if (inb && (landwin || !inwin)) bad = mask_n[succ] != 0;        // landed in obstacle
-                        if (!bad && gate) bad = seg_blocked<FLAGS>(K, t, x0, y0, x1, y1);  // transit
-                        viol |= (!bad && !inwin);
-                        const bool hit = !bad && succ == K.tcell;
-                        double rw;
-                        if (K.obj == FM_OBJ_NET_ENERGY) {
-                            const double gd = inb ? __ldg(g_n + succ) : 0.0;
-                            const double b = DMUL(DADD(AB, DMUL(K.h_cr, gd)), K.dt);
-                            rw = hit ? DADD(b, K.r_term) : b;
-                        } else {
-                            rw = hit ? base_hit : base;
-                        }
-                        int slot = (dj + K.hy) * K.width + (di + K.hx);
-                        if (bad || !inwin) slot = nslot;
-                        if (bad) rw = K.r_out;
-                        if (dead) {
-                            slot = nslot;
-                            rw = dead_r;
-                        }
-                        S = DADD(S, rw);
-                        hist[(slot >> 1) * 32 + lane] += 1u << ((slot & 1) << 4);
+                    int k = 0;
+                    for (; k + 4 <= nk; k += 4) {
+                        const double2 v0 = vbuf[vb + k], v1 = vbuf[vb + k + 1];
+                        const double2 v2 = vbuf[vb + k + 2], v3 = vbuf[vb + k + 3];
+                        int s0, s1, s2, s3;
+                        double w0, w1, w2, w3;
+                        FM_STEP(v0, s0, w0)
+                        FM_STEP(v1, s1, w1)
+                        FM_STEP(v2, s2, w2)
+                        FM_STEP(v3, s3, w3)
+                        S = DADD(S, w0);   // ascending realization order
+                        S = DADD(S, w1);
+                        S = DADD(S, w2);
+                        S = DADD(S, w3);
+                        FM_HIST(s0);
+                        FM_HIST(s1);
+                        FM_HIST(s2);
+                        FM_HIST(s3);
+                    }
+                    for (; k < nk; ++k) {
+                        const double2 v0 = vbuf[vb + k];
+                        int s0;
+                        double w0;
+                        FM_STEP(v0, s0, w0)
+                        S = DADD(S, w0);
+                        FM_HIST(s0);
                     }
                 }
+                buf ^= 1;
                 __syncwarp();
             }
+#undef FM_STEP
+#undef FM_HIST
         }
 
         if (__any_sync(kFull, viol) && viol && row_ok) atomicOr(K.viol + (size_t)t * K.na + a, 1u);
@@ -507,7 +620,7 @@ __global__ void __launch_bounds__(128) k_build(const BuildK K)
             const size_t row = ((size_t)t * K.nc + c) * K.na + a;
             K.row_ptr[row] = pos;
             K.row_nnz[row] = (uint16_t)nnz;
-            K.reward[row] = DDIV(S, (double)K.nr);   // finalize_rewards (model_builder.py:462-464)
+            K.reward[row] = DDIV(S, (double)nr);   // finalize_rewards (model_builder.py:462-464)
             for (int w = 0; w < K.hw; ++w) {
                 const uint32_t x = hist[w * 32 + lane];
                 if (!x) continue;
@@ -530,9 +643,10 @@ __global__ void __launch_bounds__(128) k_build(const BuildK K)
 // Recomputes one (t, a) sweep over every (r, c) of the layer to reproduce
 // the reference's ContractViolation message (model_builder.py:430-438):
 // argmax over non-sink entries of |di|+|dj|, first flat index r*N_c + c.
-template <int FLAGS>
-__global__ void k_viol_report(const BuildK K, int t, int a, int pass, unsigned long long *best, int32_t *didj)
+__global__ void k_viol_report(const BuildK *__restrict__ Kg, int t, int a, int pass, unsigned long long *best,
+                              int32_t *didj)
 {
+    const BuildK &K = *Kg;
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (long long)K.nr * K.nc) return;
     const int r = (int)(idx / K.nc), c = (int)(idx % K.nc);
@@ -547,12 +661,9 @@ __global__ void k_viol_report(const BuildK K, int t, int a, int pass, unsigned l
     const fm_action A = K.act[a];
     const double x0 = DADD(K.ox, DMUL(DADD((double)ci, 0.5), K.dx));
     const double y0 = DADD(K.oy, DMUL(DADD((double)cj, 0.5), K.dx));
-    double px = DADD(vx, A.ax), py = DADD(vy, A.ay);
-    px = DMUL(px, K.dt);
-    py = DMUL(py, K.dt);
-    const double x1 = DADD(x0, px), y1 = DADD(y0, py);
-    const int i1 = __double2int_rd(DDIV(DSUB(x1, K.ox), K.dx));
-    const int j1 = __double2int_rd(DDIV(DSUB(y1, K.oy), K.dx));
+    const double x1 = DADD(x0, DMUL(DADD(vx, A.ax), K.dt)), y1 = DADD(y0, DMUL(DADD(vy, A.ay), K.dt));
+    const int i1 = __double2int_rd(to_cell<0>(x1, K.ox, K.dx, K.inv_dx));
+    const int j1 = __double2int_rd(to_cell<0>(y1, K.oy, K.dx, K.inv_dx));
     const bool inb = (unsigned)i1 < (unsigned)K.nx && (unsigned)j1 < (unsigned)K.ny;
     bool bad = !inb;
     if (inb) bad = K.mask[(size_t)(t + 1) * K.nc + j1 * K.nx + i1] != 0;
@@ -570,30 +681,30 @@ __global__ void k_viol_report(const BuildK K, int t, int a, int pass, unsigned l
     }
 }
 
-static int32_t launch_build(const BuildK &K, int nm, int flags, size_t smem, int blocks, cudaStream_t s)
+template <int FL>
+static int32_t launch_build_t(const BuildK &K, const BuildK *Kg, size_t smem, cudaStream_t s)
 {
-#define FM_BUILD_CASE(NMX, FL)                                                                 \
-    if (nmx == NMX && flags == FL) {                                                           \
-        auto kern = k_build<NMX, FL>;                                                          \
-        FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        int occ = 0;                                                                           \
-        FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));          \
-        if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", smem); \
-        int nb = blocks > 0 ? blocks : occ * sm_count();                                       \
-        kern<<<nb, 128, smem, s>>>(K);                                                         \
-        FM_CK_LAUNCH("k_build");                                                               \
-        return FM_OK;                                                                          \
+    auto kern = k_build<FL>;
+    FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));
+    if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", smem);
+    kern<<<occ * sm_count(), 128, smem, s>>>(K, Kg);
+    FM_CK_LAUNCH("k_build");
+    return FM_OK;
+}
+
+static int32_t launch_build(const BuildK &K, const BuildK *Kg, int flags, size_t smem, cudaStream_t s)
+{
+    switch (flags) {
+#define FM_CASE(F) \
+    case F: return launch_build_t<F>(K, Kg, smem, s);
+        FM_CASE(0) FM_CASE(1) FM_CASE(2) FM_CASE(3) FM_CASE(4) FM_CASE(5) FM_CASE(6) FM_CASE(7)
+        FM_CASE(8) FM_CASE(9) FM_CASE(10) FM_CASE(11) FM_CASE(16) FM_CASE(17) FM_CASE(18) FM_CASE(19)
+        FM_CASE(20) FM_CASE(21) FM_CASE(22) FM_CASE(23) FM_CASE(24) FM_CASE(25) FM_CASE(26) FM_CASE(27)
+#undef FM_CASE
     }
-#define FM_BUILD_NM(NMX) \
-    FM_BUILD_CASE(NMX, 0) FM_BUILD_CASE(NMX, 1) FM_BUILD_CASE(NMX, 2) FM_BUILD_CASE(NMX, 3) \
-    FM_BUILD_CASE(NMX, 4) FM_BUILD_CASE(NMX, 5) FM_BUILD_CASE(NMX, 6) FM_BUILD_CASE(NMX, 7)
-    const int nmx = nm <= 4 ? 4 : (nm <= 8 ? 8 : 16);
-    FM_BUILD_NM(4)
-    FM_BUILD_NM(8)
-    FM_BUILD_NM(16)
-#undef FM_BUILD_NM
-#undef FM_BUILD_CASE
-    return fm_fail(FM_BAD_ARG, "k_build: unsupported n_modes %d", nm);
+    return fm_fail(FM_BAD_ARG, "k_build: bad flags %d", flags);
 }
 
 static bool is_pow2(double x)
@@ -604,6 +715,8 @@ static bool is_pow2(double x)
     return m == 0.5;
 }
 
+static int align16(int x) { return (x + 15) & ~15; }
+
 extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_needed, fm_violation *h_viol,
                             void *stream)
 {
@@ -611,7 +724,7 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
     const fm_grid &G = h->grid;
     if (G.nx < 1 || G.ny < 1 || G.nt < 1 || !(G.dx > 0) || !(G.dt > 0))
         return fm_fail(FM_BAD_ARG, "fm_build: bad grid");
-    if (h->env.n_modes < 0 || h->env.n_modes > 16) return fm_fail(FM_BAD_ARG, "fm_build: n_modes must be in [0,16]");
+    if (h->env.n_modes < 0 || h->env.n_modes > 64) return fm_fail(FM_BAD_ARG, "fm_build: n_modes must be in [0,64]");
     if (h->env.n_real < 1 || h->env.n_real > 65535) return fm_fail(FM_BAD_ARG, "fm_build: n_real must be in [1,65535]");
     if (h->n_actions < 1) return fm_fail(FM_BAD_ARG, "fm_build: need >= 1 action");
     if (h->hx < 0 || h->hy < 0) return fm_fail(FM_BAD_ARG, "fm_build: negative sub-grid");
@@ -621,20 +734,20 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
         return fm_fail(FM_BAD_ARG, "fm_build: bad slab/strip range");
     if (M->n_actions != h->n_actions || M->nt != G.nt || M->nx != G.nx || M->ny != G.ny)
         return fm_fail(FM_BAD_ARG, "fm_build: model header does not match the problem");
+    if (h->reward.target_i < 0 || h->reward.target_i >= G.nx || h->reward.target_j < 0 || h->reward.target_j >= G.ny)
+        return fm_fail(FM_BAD_ARG, "target cell (%d, %d) outside grid", h->reward.target_i, h->reward.target_j);
 
     BuildK K;
     K.nx = G.nx; K.ny = G.ny; K.nt = G.nt; K.nc = G.nx * G.ny;
     K.dx = G.dx; K.dt = G.dt; K.ox = G.ox; K.oy = G.oy;
     K.inv_dx = 1.0 / G.dx;
-    K.half_dx = 0.5 * G.dx;
+    K.half_dx = 0.5 * G.dx;   // `0.5 * grid.dx` (environment.py:356)
     K.mean = h->env.mean; K.modes = h->env.modes; K.coeffs = h->env.coeffs; K.g = h->env.g;
     K.mask = h->env.mask; K.sat = h->mask_sat;
     K.nm = h->env.n_modes; K.nr = h->env.n_real;
     K.act = h->actions; K.na = h->n_actions; K.obj = h->reward.objective;
     K.h_cr = 0.5 * h->reward.c_r;   // `0.5 * rcfg.c_r` (model_builder.py:358)
     K.r_term = h->reward.r_term; K.r_out = h->reward.r_outbound;
-    if (h->reward.target_i < 0 || h->reward.target_i >= G.nx || h->reward.target_j < 0 || h->reward.target_j >= G.ny)
-        return fm_fail(FM_BAD_ARG, "target cell (%d, %d) outside grid", h->reward.target_i, h->reward.target_j);
     K.tcell = h->reward.target_j * G.nx + h->reward.target_i;
     K.hx = h->hx; K.hy = h->hy; K.width = 2 * h->hx + 1; K.nslot = (int)nslot;
     K.hw = (int)((nslot + 2) / 2);
@@ -648,6 +761,11 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
     K.groups = (K.ncell + K.CW - 1) / K.CW;
     K.n_tasks = (long long)(h->t1 - h->t0) * K.groups * K.nag;
     if (K.n_tasks > 0xFFFFFFF0LL) return fm_fail(FM_BAD_ARG, "fm_build: too many tasks");
+    // per-warp shared memory: histogram | v chunk | coefficient double buffer | modes
+    K.off_vbuf = align16(K.hw * 128);
+    K.off_coef = K.off_vbuf + 32 * (int)sizeof(double2);
+    K.off_modes = align16(K.off_coef + 2 * K.RW * K.nm * (int)sizeof(double));
+    K.smem_warp = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
     K.entries = M->entries; K.capacity = M->capacity;
     K.nnz_counter = reinterpret_cast<unsigned long long *>(M->d_nnz);
@@ -656,11 +774,16 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
     int flags = 0;
     if (G.dt == 1.0) flags |= F_DT_ONE;
     if (G.ox == 0.0 && G.oy == 0.0) flags |= F_OX_ZERO;
-    if (is_pow2(G.dx)) flags |= F_DX_MUL;
+    if (G.dx == 1.0) flags |= F_DX_ONE;
+    else if (is_pow2(G.dx)) flags |= F_DX_MUL;
+    if (K.obj == FM_OBJ_NET_ENERGY) flags |= F_NET;
 
+    BuildK *Kg = nullptr;
+    FM_CK(cudaMallocAsync(&Kg, sizeof(BuildK), s));
+    FM_CK(cudaMemcpyAsync(Kg, &K, sizeof(BuildK), cudaMemcpyHostToDevice, s));
     FM_CK(cudaMemsetAsync(h->task_counter, 0, sizeof(unsigned int), s));
-    const size_t smem = (size_t)4 * ((size_t)K.hw * 128 + 32 * sizeof(double2));
-    int32_t st = launch_build(K, K.nm, flags, smem, 0, s);
+    const size_t smem = (size_t)4 * K.smem_warp;
+    int32_t st = launch_build(K, Kg, flags, smem, s);
     if (st != FM_OK) return st;
 
     // census + violation flags back to the host (the reference raises
@@ -675,18 +798,18 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
             if (!flags_h[(size_t)t * h->n_actions + a]) continue;
             // reproduce the reference message for the first (t, a)
             unsigned long long *d_best;
-            int32_t *d_didj;
             FM_CK(cudaMallocAsync(&d_best, sizeof(unsigned long long) + 2 * sizeof(int32_t), s));
-            d_didj = reinterpret_cast<int32_t *>(d_best + 1);
+            int32_t *d_didj = reinterpret_cast<int32_t *>(d_best + 1);
             FM_CK(cudaMemsetAsync(d_best, 0, sizeof(unsigned long long) + 2 * sizeof(int32_t), s));
             const long long n = (long long)K.nr * K.nc;
             const unsigned nb = (unsigned)((n + 255) / 256);
-            k_viol_report<0><<<nb, 256, 0, s>>>(K, t, a, 0, d_best, d_didj);
-            k_viol_report<0><<<nb, 256, 0, s>>>(K, t, a, 1, d_best, d_didj);
+            k_viol_report<<<nb, 256, 0, s>>>(Kg, t, a, 0, d_best, d_didj);
+            k_viol_report<<<nb, 256, 0, s>>>(Kg, t, a, 1, d_best, d_didj);
             FM_CK_LAUNCH_N("k_viol_report", 2);
             int32_t didj[2] = {0, 0};
             FM_CK(cudaMemcpyAsync(didj, d_didj, sizeof(didj), cudaMemcpyDeviceToHost, s));
             FM_CK(cudaFreeAsync(d_best, s));
+            FM_CK(cudaFreeAsync(Kg, s));
             FM_CK(cudaStreamSynchronize(s));
             if (h_viol) {
                 h_viol->t = t; h_viol->a = a; h_viol->di = didj[0]; h_viol->dj = didj[1];
@@ -695,6 +818,7 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
                            "displacement (%d,%d) at t=%d, a=%d exceeds sub-grid half widths (%d,%d)",
                            didj[0], didj[1], t, a, h->hx, h->hy);
         }
+    FM_CK(cudaFreeAsync(Kg, s));
     if (h_needed) *h_needed = nnz;
     if (nnz > M->capacity)
         return fm_fail(FM_CAPACITY, "fm_build: entry capacity %llu < %llu needed",
