@@ -242,7 +242,7 @@ extern "C" int32_t fm_mask_sat(const uint8_t *mask, int32_t nt, int32_t ny, int3
 // K_build
 // ---------------------------------------------------------------------------
 enum : int { F_DT_ONE = 1, F_OX_ZERO = 2, F_DX_MUL = 4, F_DX_ONE = 8, F_NET = 16 };
-enum : int { RF_DEAD = 1, RF_TERMINAL = 2, RF_GATE = 4, RF_LANDWIN = 8 };
+enum : int { RF_DEAD = 1, RF_TERMINAL = 2, RF_GATE = 4, RF_LANDWIN = 8, RF_SEGWIN = 16 };
 
 struct BuildK {
     // grid
@@ -338,11 +338,11 @@ struct SlowOut {
     int viol;
 };
 
-// Every transition the fast path cannot prove ordinary: landing outside the
-// row's clipped window (domain exit or sub-grid overflow), rows near an
-// obstacle (landing / transit tests), dead source cells.  Reads its
-// parameters from a global copy of BuildK so the call does not force the
-// kernel-parameter block onto the stack.
+// Transitions the inline tiers cannot settle: an in-domain landing outside
+// the sub-grid window (a sub-grid violation candidate) -- the full
+// reference logic of step_flat + transition_sweep (model_builder.py:331-452).
+// Reads its parameters from a global copy of BuildK so the call does not
+// force the kernel-parameter block onto the stack.
 template <int FLAGS>
 __device__ __noinline__ SlowOut slow_step(const BuildK *__restrict__ Kg, int t, int ci, int cj, double x0, double y0,
                                           double x1, double y1, int i1, int j1, int rflags, double AB, double base,
@@ -354,8 +354,8 @@ __device__ __noinline__ SlowOut slow_step(const BuildK *__restrict__ Kg, int t, 
     const bool inwin = (unsigned)(di + K.hx) <= (unsigned)(2 * K.hx) && (unsigned)(dj + K.hy) <= (unsigned)(2 * K.hy);
     const int succ = j1 * K.nx + i1;
     bool bad = !inb;
-    if (inb && ((rflags & RF_LANDWIN) || !inwin)) bad = K.mask[(size_t)(t + 1) * K.nc + succ] != 0;  // landed
-    if (!bad && (rflags & RF_GATE)) bad = seg_blocked<FLAGS>(K, t, x0, y0, x1, y1);                    // transit
+    if (inb) bad = K.mask[(size_t)(t + 1) * K.nc + succ] != 0;                      // landed in an obstacle
+    if (!bad && (rflags & RF_GATE)) bad = seg_blocked<FLAGS>(K, t, x0, y0, x1, y1);  // transit
     SlowOut o;
     o.viol = (!bad && !inwin);
     const bool hit = !bad && succ == K.tcell;
@@ -368,11 +368,14 @@ __device__ __noinline__ SlowOut slow_step(const BuildK *__restrict__ Kg, int t, 
     }
     o.slot = (bad || !inwin) ? K.nslot : (dj + K.hy) * K.width + (di + K.hx);
     if (bad) o.rw = K.r_out;
-    if (rflags & RF_DEAD) {   // after the overflow check (model_builder.py:445-452)
-        o.slot = K.nslot;
-        o.rw = (rflags & RF_TERMINAL) ? 0.0 : K.r_out;
-    }
     return o;
+}
+
+template <int FLAGS>
+__device__ __noinline__ bool seg_blocked_call(const BuildK *__restrict__ Kg, int t, double p0x, double p0y, double p1x,
+                                              double p1y)
+{
+    return seg_blocked<FLAGS>(*Kg, t, p0x, p0y, p1x, p1y);
 }
 
 __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src)
@@ -382,6 +385,110 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src)
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// Per-row constants of one task (registers).
+struct RowC {
+    double x0, y0, ax, ay, base, base_hit, AB;
+    int ci, cj, ilc, jlc, wi, wj, soff, tslot, rflags;
+};
+
+// One transition of one row (step_flat + the slot / dead logic of
+// transition_sweep).  OBST = some row of this warp is dead or has an
+// obstacle cell near it; otherwise none of the obstacle tests can fire and
+// the lean variant is exact.
+//   tier 1: landing inside the row's grid-clipped sub-grid window
+//   tier 2: landing outside the domain -> SINK, r_outbound
+//   tier 3: in-domain landing outside the window -> slow_step
+template <int FLAGS, bool OBST>
+__device__ __forceinline__ void step_one(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
+                                         const double2 v, const double *__restrict__ g_n,
+                                         const uint8_t *__restrict__ mask_n, int &slot, double &rw, int &viol)
+{
+    double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
+    if (!(FLAGS & F_DT_ONE)) {
+        px = DMUL(px, K.dt);
+        py = DMUL(py, K.dt);
+    }
+    const double x1 = DADD(R.x0, px), y1 = DADD(R.y0, py);
+    const int i1 = __double2int_rd(to_cell<FLAGS>(x1, K.ox, K.dx, K.inv_dx));
+    const int j1 = __double2int_rd(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx));
+    if ((unsigned)(i1 - R.ilc) <= (unsigned)R.wi && (unsigned)(j1 - R.jlc) <= (unsigned)R.wj) {
+        slot = j1 * K.width + i1 + R.soff;
+        bool bad = false;
+        if (OBST) {
+            if (R.rflags & RF_LANDWIN) bad = mask_n[j1 * K.nx + i1] != 0;
+            if (!bad && (R.rflags & RF_SEGWIN)) {
+                // every sample cell of the segment lies within one cell of the
+                // box spanned by the source and landing cells
+                if (box_count(K, t, min(R.ci, i1) - 1, max(R.ci, i1) + 1, min(R.cj, j1) - 1, max(R.cj, j1) + 1) > 0)
+                    bad = seg_blocked_call<FLAGS>(Kg, t, R.x0, R.y0, x1, y1);
+            }
+        }
+        const bool hit = !bad && slot == R.tslot;
+        if (FLAGS & F_NET) {
+            const double gd = __ldg(g_n + j1 * K.nx + i1);
+            double b = DADD(R.AB, DMUL(K.h_cr, gd));
+            if (!(FLAGS & F_DT_ONE)) b = DMUL(b, K.dt);
+            rw = hit ? DADD(b, K.r_term) : b;
+        } else {
+            rw = hit ? R.base_hit : R.base;
+        }
+        if (OBST && bad) {
+            slot = K.nslot;
+            rw = K.r_out;
+        }
+    } else if ((unsigned)i1 >= (unsigned)K.nx || (unsigned)j1 >= (unsigned)K.ny) {
+        slot = K.nslot;   // left the domain
+        rw = K.r_out;
+    } else {
+        const SlowOut o = slow_step<FLAGS>(Kg, t, R.ci, R.cj, R.x0, R.y0, x1, y1, i1, j1, R.rflags, R.AB, R.base,
+                                           R.base_hit);
+        slot = o.slot;
+        rw = o.rw;
+        viol |= o.viol;
+    }
+    if (OBST && (R.rflags & RF_DEAD)) {   // after the overflow check (model_builder.py:445-452)
+        slot = K.nslot;
+        rw = (R.rflags & RF_TERMINAL) ? 0.0 : K.r_out;
+    }
+}
+
+#define FM_HIST(SLOT) hist[((SLOT) >> 1) * 32 + lane] += 1u << (((SLOT) & 1) << 4)
+
+// The realization loop of one chunk for the row lanes: 4 transitions per
+// iteration with their v loads hoisted, reward sums in ascending r order.
+template <int FLAGS, bool OBST>
+__device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
+                                           const double2 *vrow, int nk, const double *__restrict__ g_n,
+                                           const uint8_t *__restrict__ mask_n, uint32_t *hist, int lane, double &S,
+                                           int &viol)
+{
+    int k = 0;
+    for (; k + 4 <= nk; k += 4) {
+        const double2 v0 = vrow[k], v1 = vrow[k + 1], v2 = vrow[k + 2], v3 = vrow[k + 3];
+        int s0, s1, s2, s3;
+        double w0, w1, w2, w3;
+        step_one<FLAGS, OBST>(K, Kg, t, R, v0, g_n, mask_n, s0, w0, viol);
+        step_one<FLAGS, OBST>(K, Kg, t, R, v1, g_n, mask_n, s1, w1, viol);
+        step_one<FLAGS, OBST>(K, Kg, t, R, v2, g_n, mask_n, s2, w2, viol);
+        step_one<FLAGS, OBST>(K, Kg, t, R, v3, g_n, mask_n, s3, w3, viol);
+        S = DADD(S, w0);   // ascending realization order (model_builder.py:457-458)
+        S = DADD(S, w1);
+        S = DADD(S, w2);
+        S = DADD(S, w3);
+        FM_HIST(s0);
+        FM_HIST(s1);
+        FM_HIST(s2);
+        FM_HIST(s3);
+    }
+    for (; k < nk; ++k) {
+        int s0;
+        double w0;
+        step_one<FLAGS, OBST>(K, Kg, t, R, vrow[k], g_n, mask_n, s0, w0, viol);
+        S = DADD(S, w0);
+        FM_HIST(s0);
+    }
+}
 
 // One warp = one task (t, group of CW source cells, group of <=32 actions).
 // Lane roles:
@@ -429,43 +536,53 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
         const int lc_row = grp * CW + cs_row;
         const bool row_ok = row_lane && lc_row < K.ncell && a < K.na;
         const int c = K.cell0 + lc_row;
-        const int ci = c % K.nx, cj = c / K.nx;
         const bool horizon = (t + 1 >= K.nt);
 
         // ---- per-row constants
-        double x0 = 0, y0 = 0, ax = 0, ay = 0, base = 0, base_hit = 0, AB = 0;
-        int rflags = RF_DEAD, ilc = 0, jlc = 0, wi = -1, wj = -1, soff = 0, tslot = -1;
+        RowC R;
+        R.ci = c % K.nx;
+        R.cj = c / K.nx;
+        R.x0 = R.y0 = R.ax = R.ay = R.base = R.base_hit = R.AB = 0.0;
+        R.ilc = R.jlc = R.soff = 0;
+        R.wi = R.wj = R.tslot = -1;
+        R.rflags = 0;
         bool terminal = false;
         if (row_ok) {
-            x0 = DADD(K.ox, DMUL(DADD((double)ci, 0.5), K.dx));   // environment.py:99-100
-            y0 = DADD(K.oy, DMUL(DADD((double)cj, 0.5), K.dx));
+            const int ci = R.ci, cj = R.cj;
+            R.x0 = DADD(K.ox, DMUL(DADD((double)ci, 0.5), K.dx));   // environment.py:99-100
+            R.y0 = DADD(K.oy, DMUL(DADD((double)cj, 0.5), K.dx));
             const fm_action A = K.act[a];
-            ax = A.ax;
-            ay = A.ay;
-            base = A.base;
-            base_hit = A.base_hit;
+            R.ax = A.ax;
+            R.ay = A.ay;
+            R.base = A.base;
+            R.base_hit = A.base_hit;
             terminal = (c == K.tcell);
             const bool obstacle = !terminal && K.mask[(size_t)t * K.nc + c];
-            rflags = (terminal || obstacle) ? RF_DEAD : 0;
-            if (terminal) rflags |= RF_TERMINAL;
+            if (terminal || obstacle) R.rflags |= RF_DEAD;
+            if (terminal) R.rflags |= RF_TERMINAL;
             if (!horizon) {
-                if (box_count(K, t, ci - K.rx, ci + K.rx, cj - K.ry, cj + K.ry) > 0) rflags |= RF_GATE;
-                if (box_count(K, t + 1, ci - K.hx, ci + K.hx, cj - K.hy, cj + K.hy) > 0) rflags |= RF_LANDWIN;
+                // the reference's obstacle gate (model_builder.py:218-228, 339-345)
+                if (box_count(K, t, ci - K.rx, ci + K.rx, cj - K.ry, cj + K.ry) > 0) {
+                    R.rflags |= RF_GATE;
+                    // an in-window segment only touches cells within one of the window
+                    if (box_count(K, t, ci - K.hx - 1, ci + K.hx + 1, cj - K.hy - 1, cj + K.hy + 1) > 0)
+                        R.rflags |= RF_SEGWIN;
+                }
+                if (box_count(K, t + 1, ci - K.hx, ci + K.hx, cj - K.hy, cj + K.hy) > 0) R.rflags |= RF_LANDWIN;
                 if (K.obj == FM_OBJ_NET_ENERGY)
-                    AB = DADD(A.neg_cff, DMUL(K.h_cr, K.g[(size_t)t * K.nc + c]));   // model_builder.py:358
+                    R.AB = DADD(A.neg_cff, DMUL(K.h_cr, K.g[(size_t)t * K.nc + c]));   // model_builder.py:358
             }
             // window [ci-hx, ci+hx] x [cj-hy, cj+hy] clipped to the grid: a
             // landing inside it is in-domain and inside the sub-grid
-            ilc = max(ci - K.hx, 0);
-            jlc = max(cj - K.hy, 0);
-            wi = min(ci + K.hx, K.nx - 1) - ilc;
-            wj = min(cj + K.hy, K.ny - 1) - jlc;
-            soff = -((cj - K.hy) * W + (ci - K.hx));    // slot = j1*W + i1 + soff
+            R.ilc = max(ci - K.hx, 0);
+            R.jlc = max(cj - K.hy, 0);
+            R.wi = min(ci + K.hx, K.nx - 1) - R.ilc;
+            R.wj = min(cj + K.hy, K.ny - 1) - R.jlc;
+            R.soff = -((cj - K.hy) * W + (ci - K.hx));    // slot = j1*W + i1 + soff
             const int tci = K.tcell % K.nx, tcj = K.tcell / K.nx;
-            if ((unsigned)(tci - ilc) <= (unsigned)wi && (unsigned)(tcj - jlc) <= (unsigned)wj)
-                tslot = tcj * W + tci + soff;
+            if ((unsigned)(tci - R.ilc) <= (unsigned)R.wi && (unsigned)(tcj - R.jlc) <= (unsigned)R.wj)
+                R.tslot = tcj * W + tci + R.soff;
         }
-        const bool row_clear = row_ok && rflags == 0;
         double S = 0.0;
         int viol = 0;
 
@@ -478,6 +595,7 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
                 hist[(nslot >> 1) * 32 + lane] = (uint32_t)nr << ((nslot & 1) << 4);
             }
         } else {
+            const bool obst = __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
             // stage the CW cells' modes, issue chunk 0's coefficients
             for (int i = lane; i < CW * nm; i += 32) {
                 const int cs = i / nm, m = i - (i / nm) * nm;
@@ -497,43 +615,9 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
             }
             cp_async_commit();
             const double *g_n = K.g + (size_t)(t + 1) * K.nc;
-            const int vb = cs_row * RW;
-            const double dt = K.dt, ox = K.ox, oy = K.oy, dx = K.dx, inv_dx = K.inv_dx;
-            const double h_cr = K.h_cr, r_term = K.r_term;
-            const int nx = K.nx;
+            const uint8_t *mask_n = K.mask + (size_t)(t + 1) * K.nc;
+            const double2 *vrow = vbuf + cs_row * RW;
             int buf = 0;
-
-#define FM_STEP(V, SLOT, RWV)                                                                          \
-    {                                                                                                  \
-        double px_ = DADD((V).x, ax), py_ = DADD((V).y, ay);                                           \
-        if (!(FLAGS & F_DT_ONE)) {                                                                     \
-            px_ = DMUL(px_, dt);                                                                       \
-            py_ = DMUL(py_, dt);                                                                       \
-        }                                                                                              \
-        const double x1_ = DADD(x0, px_), y1_ = DADD(y0, py_);                                         \
-        const int i1_ = __double2int_rd(to_cell<FLAGS>(x1_, ox, dx, inv_dx));                          \
-        const int j1_ = __double2int_rd(to_cell<FLAGS>(y1_, oy, dx, inv_dx));                          \
-        if (row_clear && (unsigned)(i1_ - ilc) <= (unsigned)wi && (unsigned)(j1_ - jlc) <= (unsigned)wj) { \
-            SLOT = j1_ * W + i1_ + soff;                                                               \
-            const bool hit_ = SLOT == tslot;                                                           \
-            if (FLAGS & F_NET) {                                                                       \
-                const double gd_ = __ldg(g_n + j1_ * nx + i1_);                                        \
-                double b_ = DADD(AB, DMUL(h_cr, gd_));                                                 \
-                if (!(FLAGS & F_DT_ONE)) b_ = DMUL(b_, dt);                                            \
-                RWV = hit_ ? DADD(b_, r_term) : b_;                                                    \
-            } else {                                                                                   \
-                RWV = hit_ ? base_hit : base;                                                          \
-            }                                                                                          \
-        } else {                                                                                       \
-            const SlowOut o_ = slow_step<FLAGS>(Kg, t, ci, cj, x0, y0, x1_, y1_, i1_, j1_, rflags, AB, \
-                                                base, base_hit);                                       \
-            SLOT = o_.slot;                                                                            \
-            RWV = o_.rw;                                                                               \
-            viol |= o_.viol;                                                                           \
-        }                                                                                              \
-    }
-#define FM_HIST(SLOT) hist[((SLOT) >> 1) * 32 + lane] += 1u << (((SLOT) & 1) << 4)
-
             for (int r0 = 0; r0 < nr; r0 += RW) {
                 // prefetch the next chunk's coefficients into the other buffer
                 if (r0 + RW < nr) {
@@ -561,39 +645,14 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
                 __syncwarp();
                 const int nk = min(RW, nr - r0);
                 if (row_ok) {
-                    int k = 0;
-                    for (; k + 4 <= nk; k += 4) {
-                        const double2 v0 = vbuf[vb + k], v1 = vbuf[vb + k + 1];
-                        const double2 v2 = vbuf[vb + k + 2], v3 = vbuf[vb + k + 3];
-                        int s0, s1, s2, s3;
-                        double w0, w1, w2, w3;
-                        FM_STEP(v0, s0, w0)
-                        FM_STEP(v1, s1, w1)
-                        FM_STEP(v2, s2, w2)
-                        FM_STEP(v3, s3, w3)
-                        S = DADD(S, w0);   // ascending realization order
-                        S = DADD(S, w1);
-                        S = DADD(S, w2);
-                        S = DADD(S, w3);
-                        FM_HIST(s0);
-                        FM_HIST(s1);
-                        FM_HIST(s2);
-                        FM_HIST(s3);
-                    }
-                    for (; k < nk; ++k) {
-                        const double2 v0 = vbuf[vb + k];
-                        int s0;
-                        double w0;
-                        FM_STEP(v0, s0, w0)
-                        S = DADD(S, w0);
-                        FM_HIST(s0);
-                    }
+                    if (obst)
+                        chunk_rows<FLAGS, true>(K, Kg, t, R, vrow, nk, g_n, mask_n, hist, lane, S, viol);
+                    else
+                        chunk_rows<FLAGS, false>(K, Kg, t, R, vrow, nk, g_n, mask_n, hist, lane, S, viol);
                 }
                 buf ^= 1;
                 __syncwarp();
             }
-#undef FM_STEP
-#undef FM_HIST
         }
 
         if (__any_sync(kFull, viol) && viol && row_ok) atomicOr(K.viol + (size_t)t * K.na + a, 1u);
