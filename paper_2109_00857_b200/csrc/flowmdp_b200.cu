@@ -263,7 +263,7 @@ struct BuildK {
     int rx, ry;
     // task decomposition
     int t0, t1, cell0, ncell;   // strip = cells [cell0, cell0 + ncell) of each layer
-    int CW, RW, AG, nag, groups;
+    int CW, RW, AG, nag, groups, RC;
     long long n_tasks;
     // per-warp shared-memory carve-up (bytes)
     int smem_warp, off_vbuf, off_coef, off_modes;
@@ -384,7 +384,7 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Per-row constants of one task (registers).
 struct RowC {
@@ -453,15 +453,15 @@ __device__ __forceinline__ void step_one(const BuildK &K, const BuildK *__restri
     }
 }
 
-#define FM_HIST(SLOT) hist[((SLOT) >> 1) * 32 + lane] += 1u << (((SLOT) & 1) << 4)
+// u16 counters laid out [slot][lane]: one IMAD + LDS.U16 + IADD + STS.U16
+#define FM_HIST(SLOT) h16[(SLOT) * 32] += (uint16_t)1
 
 // The realization loop of one chunk for the row lanes: 4 transitions per
 // iteration with their v loads hoisted, reward sums in ascending r order.
 template <int FLAGS, bool OBST>
 __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
                                            const double2 *vrow, int nk, const double *__restrict__ g_n,
-                                           const uint8_t *__restrict__ mask_n, uint32_t *hist, int lane, double &S,
-                                           int &viol)
+                                           const uint8_t *__restrict__ mask_n, uint16_t *h16, double &S, int &viol)
 {
     int k = 0;
     for (; k + 4 <= nk; k += 4) {
@@ -508,20 +508,25 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *wbase = smem + (size_t)warp * K.smem_warp;
-    uint32_t *hist = reinterpret_cast<uint32_t *>(wbase);
-    double2 *vbuf = reinterpret_cast<double2 *>(wbase + K.off_vbuf);
-    double *coef = reinterpret_cast<double *>(wbase + K.off_coef);     // [2][RW * nm]
-    double2 *modes_s = reinterpret_cast<double2 *>(wbase + K.off_modes);  // [CW][nm]
+    uint16_t *hist16 = reinterpret_cast<uint16_t *>(wbase);                 // [nslot+1][32]
+    uint16_t *h16 = hist16 + lane;
+    double2 *vbuf = reinterpret_cast<double2 *>(wbase + K.off_vbuf);       // [CW][RC+1]
+    double *coefT = reinterpret_cast<double *>(wbase + K.off_coef);        // [nm][RC]
+    double2 *modes_s = reinterpret_cast<double2 *>(wbase + K.off_modes);   // [CW][nm]
 
-    for (int w = 0; w < K.hw; ++w) hist[w * 32 + lane] = 0u;
+    for (int sl = 0; sl <= K.nslot; ++sl) h16[sl * 32] = 0;
 
     const int AG = K.AG, RW = K.RW, CW = K.CW, nm = K.nm, nr = K.nr;
+    const int RC = K.RC, RPL = RC / RW;
     const int cs_row = lane / AG, a_loc = lane - cs_row * AG;
     const bool row_lane = lane < CW * AG;
     const int cs_rec = lane / RW, rr = lane - cs_rec * RW;
     const bool rec_lane = lane < CW * RW;
     const int nslot = K.nslot, W = K.width;
-    const int coef_stride = RW * nm;
+    // this lane's first (realization, mode) element of a coefficient chunk and
+    // the per-step increments (element index advances by 32 each step)
+    const int e_r0 = nm ? lane / nm : 0, e_m0 = nm ? lane - (lane / nm) * nm : 0;
+    const int e_dr = nm ? 32 / nm : 0, e_dm = nm ? 32 - (32 / nm) * nm : 0;
 
     for (;;) {
         unsigned task = 0;
@@ -592,11 +597,11 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
             if (row_ok) {
                 const double rw = terminal ? 0.0 : K.r_out;
                 for (int r = 0; r < nr; ++r) S = DADD(S, rw);
-                hist[(nslot >> 1) * 32 + lane] = (uint32_t)nr << ((nslot & 1) << 4);
+                h16[nslot * 32] = (uint16_t)nr;
             }
         } else {
             const bool obst = __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
-            // stage the CW cells' modes, issue chunk 0's coefficients
+            // stage the CW cells' modes
             for (int i = lane; i < CW * nm; i += 32) {
                 const int cs = i / nm, m = i - (i / nm) * nm;
                 const int lc = grp * CW + cs;
@@ -609,48 +614,56 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
             double2 mu = make_double2(0.0, 0.0);
             if (rec_ok) mu = *reinterpret_cast<const double2 *>(K.mean + ((size_t)t * K.nc + K.cell0 + lc_rec) * 2);
             const double *cf_t = K.coeffs + (size_t)t * nr * nm;
-            {
-                const int n_el = min(RW, nr) * nm;
-                for (int i = lane; i < n_el; i += 32) cp_async8(coef + i, cf_t + i);
-            }
-            cp_async_commit();
             const double *g_n = K.g + (size_t)(t + 1) * K.nc;
             const uint8_t *mask_n = K.mask + (size_t)(t + 1) * K.nc;
-            const double2 *vrow = vbuf + cs_row * RW;
-            int buf = 0;
-            for (int r0 = 0; r0 < nr; r0 += RW) {
-                // prefetch the next chunk's coefficients into the other buffer
-                if (r0 + RW < nr) {
-                    const int n_el = min(RW, nr - r0 - RW) * nm;
-                    const double *src = cf_t + (size_t)(r0 + RW) * nm;
-                    double *dst = coef + (buf ^ 1) * coef_stride;
-                    for (int i = lane; i < n_el; i += 32) cp_async8(dst + i, src + i);
+            const double2 *vrow = vbuf + cs_row * (RC + 1);
+            // chunk loader: coefficients [r0, r0+RC) x [0, nm) land transposed
+            // as coefT[m][r - r0] (conflict-free reads in the reconstruction);
+            // element-granular cp.async, contiguous (coalesced) global reads.
+            auto issue_chunk = [&](int r0) {
+                const int n_el = min(RC, nr - r0) * nm;
+                const double *src = cf_t + (size_t)r0 * nm;
+                int er = e_r0, em = e_m0;
+                for (int i = lane; i < n_el; i += 32) {
+                    cp_async8(coefT + em * RC + er, src + i);
+                    er += e_dr;
+                    em += e_dm;
+                    if (em >= nm) {
+                        em -= nm;
+                        ++er;
+                    }
                 }
                 cp_async_commit();
-                cp_async_wait1();
+            };
+            issue_chunk(0);
+            for (int r0 = 0; r0 < nr; r0 += RC) {
+                cp_async_wait_all();
                 __syncwarp();
-                const int r = r0 + rr;
-                if (rec_ok && r < nr) {
-                    const double *cf = coef + buf * coef_stride + rr * nm;
+                if (rec_ok) {
                     const double2 *md = modes_s + cs_rec * nm;
-                    double vx = mu.x, vy = mu.y;
-                    for (int m = 0; m < nm; ++m) {
-                        const double k = cf[m];
-                        const double2 mm = md[m];
-                        vx = DADD(vx, DMUL(k, mm.x));
-                        vy = DADD(vy, DMUL(k, mm.y));
+                    for (int p = 0; p < RPL; ++p) {
+                        const int rl = p * RW + rr;
+                        if (r0 + rl < nr) {
+                            double vx = mu.x, vy = mu.y;
+                            for (int m = 0; m < nm; ++m) {   // environment.py:295-297, ascending m
+                                const double k = coefT[m * RC + rl];
+                                const double2 mm = md[m];
+                                vx = DADD(vx, DMUL(k, mm.x));
+                                vy = DADD(vy, DMUL(k, mm.y));
+                            }
+                            vbuf[cs_rec * (RC + 1) + rl] = make_double2(vx, vy);
+                        }
                     }
-                    vbuf[cs_rec * RW + rr] = make_double2(vx, vy);
                 }
                 __syncwarp();
-                const int nk = min(RW, nr - r0);
+                if (r0 + RC < nr) issue_chunk(r0 + RC);   // lands while the rows work
+                const int nk = min(RC, nr - r0);
                 if (row_ok) {
                     if (obst)
-                        chunk_rows<FLAGS, true>(K, Kg, t, R, vrow, nk, g_n, mask_n, hist, lane, S, viol);
+                        chunk_rows<FLAGS, true>(K, Kg, t, R, vrow, nk, g_n, mask_n, h16, S, viol);
                     else
-                        chunk_rows<FLAGS, false>(K, Kg, t, R, vrow, nk, g_n, mask_n, hist, lane, S, viol);
+                        chunk_rows<FLAGS, false>(K, Kg, t, R, vrow, nk, g_n, mask_n, h16, S, viol);
                 }
-                buf ^= 1;
                 __syncwarp();
             }
         }
@@ -660,10 +673,7 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
         // ---- emit: nnz census, warp scan, bump allocation, slot-ordered fill
         int nnz = 0;
         if (row_ok)
-            for (int w = 0; w < K.hw; ++w) {
-                const uint32_t x = hist[w * 32 + lane];
-                nnz += ((x & 0xffffu) != 0) + ((x >> 16) != 0);
-            }
+            for (int sl = 0; sl <= nslot; ++sl) nnz += h16[sl * 32] != 0;
         int incl = nnz;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -680,19 +690,12 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
             K.row_ptr[row] = pos;
             K.row_nnz[row] = (uint16_t)nnz;
             K.reward[row] = DDIV(S, (double)nr);   // finalize_rewards (model_builder.py:462-464)
-            for (int w = 0; w < K.hw; ++w) {
-                const uint32_t x = hist[w * 32 + lane];
+            for (int sl = 0; sl <= nslot; ++sl) {
+                const uint32_t x = h16[sl * 32];
                 if (!x) continue;
-                hist[w * 32 + lane] = 0u;
-                const uint32_t lo = x & 0xffffu, hi = x >> 16;
-                if (lo) {
-                    if (pos < K.capacity) K.entries[pos] = ((uint32_t)(2 * w) << 16) | lo;
-                    ++pos;
-                }
-                if (hi) {
-                    if (pos < K.capacity) K.entries[pos] = ((uint32_t)(2 * w + 1) << 16) | hi;
-                    ++pos;
-                }
+                h16[sl * 32] = 0;
+                if (pos < K.capacity) K.entries[pos] = ((uint32_t)sl << 16) | x;   // slots ascend = cols ascend
+                ++pos;
             }
         }
         __syncwarp();
@@ -820,10 +823,13 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
     K.groups = (K.ncell + K.CW - 1) / K.CW;
     K.n_tasks = (long long)(h->t1 - h->t0) * K.groups * K.nag;
     if (K.n_tasks > 0xFFFFFFF0LL) return fm_fail(FM_BAD_ARG, "fm_build: too many tasks");
-    // per-warp shared memory: histogram | v chunk | coefficient double buffer | modes
-    K.off_vbuf = align16(K.hw * 128);
-    K.off_coef = K.off_vbuf + 32 * (int)sizeof(double2);
-    K.off_modes = align16(K.off_coef + 2 * K.RW * K.nm * (int)sizeof(double));
+    // realizations per chunk: RW recon lanes per cell, 64 realizations
+    K.RC = K.RW >= 64 ? K.RW : 64;
+    // per-warp shared memory: u16 histogram [nslot+1][32] | v chunk [CW][RC+1]
+    // | transposed coefficients [nm][RC] | modes [CW][nm]
+    K.off_vbuf = align16((int)(nslot + 1) * 64);
+    K.off_coef = K.off_vbuf + K.CW * (K.RC + 1) * (int)sizeof(double2);
+    K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
     K.smem_warp = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
     K.entries = M->entries; K.capacity = M->capacity;
