@@ -102,44 +102,104 @@ __device__ __forceinline__ void atomic_max_nonneg(double *addr, double v)
 
 // ---------------------------------------------------------------------------
 // K_vmax: compute_subgrid's exact scan (model_builder.py:392-396)
+//
+// max over (t, r, cell) of |v_x| and |v_y|, exact.  The scan runs in FP32
+// (FFMA, smem-staged coefficients) with a rigorous per-cell error bound
+//   |v32 - v| <= delta = (2 n_m + 8) 2^-24 T + tiny,
+//   T = |mean| + sum_m |mode_m| max_r |coeff_{t,r,m}|   (>= every partial sum),
+// and only elements with |v32| >= rd(E - delta), E the running exact max,
+// are recomputed in f64 with the reference's operation order.  The true
+// maximiser always passes that test, so the result is the exact f64 max;
+// recomputes happen O(log N_rv) times per cell.
 // ---------------------------------------------------------------------------
+static constexpr int kVmaxChunk = 64;
+
 template <int NMX>
-__global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int rchunk, double *out2)
+__device__ __noinline__ double vmax_exact_component(const fm_grid G, const fm_env E, int t, int r, int c, int comp)
 {
+    const int nc = G.nx * G.ny;
+    double v = E.mean[((size_t)t * nc + c) * 2 + comp];
+    const double *cf = E.coeffs + ((size_t)t * E.n_real + r) * E.n_modes;
+    for (int m = 0; m < E.n_modes; ++m)
+        v = DADD(v, DMUL(cf[m], E.modes[(((size_t)m * G.nt + t) * nc + c) * 2 + comp]));
+    return fabs(v);
+}
+
+template <int NMX>
+__global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_block, const double *cmax, double *out2)
+{
+    __shared__ float cs[kVmaxChunk][NMX];
     const int nc = G.nx * G.ny;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int t = blockIdx.y;
-    const int r_lo = blockIdx.z * rchunk;
-    const int r_hi = min(E.n_real, r_lo + rchunk);
-    double mx = 0.0, my = 0.0;
-    if (c < nc) {
+    const int nm = E.n_modes;
+    const int r_lo = blockIdx.z * r_per_block;
+    const int r_hi = min(E.n_real, r_lo + r_per_block);
+    const bool ok = c < nc;
+    float mx32 = 0.f, my32 = 0.f;
+    float dx32[NMX], dy32[NMX];
+    double Tx = 0.0, Ty = 0.0;
+    if (ok) {
         const double2 mu = *reinterpret_cast<const double2 *>(E.mean + ((size_t)t * nc + c) * 2);
-        double2 md[NMX];
+        mx32 = (float)mu.x;
+        my32 = (float)mu.y;
+        Tx = fabs(mu.x);
+        Ty = fabs(mu.y);
 #pragma unroll
-        for (int m = 0; m < NMX; ++m)
-            if (m < E.n_modes)
-                md[m] = *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + c) * 2);
-        for (int r = r_lo; r < r_hi; ++r) {
-            const double *cf = E.coeffs + ((size_t)t * E.n_real + r) * E.n_modes;
-            double vx = mu.x, vy = mu.y;
-#pragma unroll
-            for (int m = 0; m < NMX; ++m)
-                if (m < E.n_modes) {
-                    const double k = __ldg(cf + m);
-                    vx = DADD(vx, DMUL(k, md[m].x));
-                    vy = DADD(vy, DMUL(k, md[m].y));
-                }
-            mx = fmax(mx, fabs(vx));
-            my = fmax(my, fabs(vy));
+        for (int m = 0; m < NMX; ++m) {
+            dx32[m] = dy32[m] = 0.f;
+            if (m < nm) {
+                const double2 md = *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + c) * 2);
+                dx32[m] = (float)md.x;
+                dy32[m] = (float)md.y;
+                const double cm = cmax[(size_t)t * nm + m];
+                Tx += fabs(md.x) * cm;
+                Ty += fabs(md.y) * cm;
+            }
         }
     }
-    mx = warp_max_f64(mx);
-    my = warp_max_f64(my);
+    const double kRel = (2.0 * nm + 8.0) * 0x1p-24 * 1.001, kAbs = (nm + 2.0) * 0x1p-140;
+    const double delx = Tx * kRel + kAbs, dely = Ty * kRel + kAbs;
+    double ex = 0.0, ey = 0.0;                                    // running exact maxima
+    float thx = __double2float_rd(-delx), thy = __double2float_rd(-dely);
+    for (int r0 = r_lo; r0 < r_hi; r0 += kVmaxChunk) {
+        const int n = min(kVmaxChunk, r_hi - r0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < n * nm; i += blockDim.x) {
+            const int k = i / nm, m = i - (i / nm) * nm;
+            cs[k][m] = (float)E.coeffs[((size_t)t * E.n_real + r0 + k) * nm + m];
+        }
+        __syncthreads();
+        if (!ok) continue;
+        for (int k = 0; k < n; ++k) {
+            float vx = mx32, vy = my32;
+#pragma unroll
+            for (int m = 0; m < NMX; ++m)
+                if (m < nm) {
+                    const float cc = cs[k][m];
+                    vx = fmaf(cc, dx32[m], vx);
+                    vy = fmaf(cc, dy32[m], vy);
+                }
+            if (fabsf(vx) >= thx) {
+                ex = fmax(ex, vmax_exact_component<NMX>(G, E, t, r0 + k, c, 0));
+                thx = __double2float_rd(ex - delx);
+            }
+            if (fabsf(vy) >= thy) {
+                ey = fmax(ey, vmax_exact_component<NMX>(G, E, t, r0 + k, c, 1));
+                thy = __double2float_rd(ey - dely);
+            }
+        }
+    }
+    ex = warp_max_f64(ex);
+    ey = warp_max_f64(ey);
     if ((threadIdx.x & 31) == 0) {
-        atomic_max_nonneg(out2, mx);
-        atomic_max_nonneg(out2 + 1, my);
+        atomic_max_nonneg(out2, ex);
+        atomic_max_nonneg(out2 + 1, ey);
     }
 }
+
+__global__ void k_maxabs_seg(const double *src, int64_t seg_len, int64_t elem_stride, int64_t inner,
+                             int64_t outer_stride, int64_t inner_stride, double *out);
 
 extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *stream)
 {
@@ -147,24 +207,32 @@ extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *st
         return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims (n_modes must be <= 16)");
     cudaStream_t s = (cudaStream_t)stream;
     const int nc = G.nx * G.ny;
-    const int bx = (nc + 255) / 256;
-    // enough blocks to fill the machine several times over
-    long long base = (long long)bx * G.nt;
-    int rchunk = E.n_real;
-    long long want = 8LL * sm_count();
-    if (base < want) {
-        long long split = (want + base - 1) / base;
-        rchunk = (int)((E.n_real + split - 1) / split);
-        if (rchunk < 16) rchunk = 16;
+    const int nm = E.n_modes;
+    // max_r |coeff[t, r, m]| per (t, m): the error-bound ingredient
+    double *cmax = nullptr;
+    FM_CK(cudaMallocAsync(&cmax, sizeof(double) * (size_t)(G.nt * (nm > 0 ? nm : 1)), s));
+    if (nm > 0) {
+        k_maxabs_seg<<<G.nt * nm, 256, 0, s>>>(E.coeffs, E.n_real, nm, nm, (int64_t)E.n_real * nm, 1, cmax);
+        FM_CK_LAUNCH("k_maxabs_seg");
     }
-    dim3 grid(bx, G.nt, (E.n_real + rchunk - 1) / rchunk);
-    if (E.n_modes <= 4)
-        k_vmax<4><<<grid, 256, 0, s>>>(G, E, rchunk, d_out2);
-    else if (E.n_modes <= 8)
-        k_vmax<8><<<grid, 256, 0, s>>>(G, E, rchunk, d_out2);
+    const int bx = (nc + 255) / 256;
+    long long base = (long long)bx * G.nt;
+    int rpb = E.n_real;
+    const long long want = 4LL * sm_count();
+    if (base < want) {
+        const long long split = (want + base - 1) / base;
+        rpb = (int)((E.n_real + split - 1) / split);
+        rpb = ((rpb + kVmaxChunk - 1) / kVmaxChunk) * kVmaxChunk;
+    }
+    dim3 grid(bx, G.nt, (E.n_real + rpb - 1) / rpb);
+    if (nm <= 4)
+        k_vmax<4><<<grid, 256, 0, s>>>(G, E, rpb, cmax, d_out2);
+    else if (nm <= 8)
+        k_vmax<8><<<grid, 256, 0, s>>>(G, E, rpb, cmax, d_out2);
     else
-        k_vmax<16><<<grid, 256, 0, s>>>(G, E, rchunk, d_out2);
+        k_vmax<16><<<grid, 256, 0, s>>>(G, E, rpb, cmax, d_out2);
     FM_CK_LAUNCH("k_vmax");
+    FM_CK(cudaFreeAsync(cmax, s));
     return FM_OK;
 }
 

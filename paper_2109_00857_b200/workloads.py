@@ -154,6 +154,7 @@ class Workload:
     r_term: float = 100.0
     r_outbound: float = -300.0
     buffer: int = 1
+    subgrid_hint: tuple | None = None   # exact (hx, hy), pinned by tests
 
     @property
     def n_actions(self) -> int:
@@ -203,12 +204,13 @@ WORKLOADS = {
                       obstacles=(2, 0, 0.0, ((4, 4),)), n_headings=8, n_speeds=2, f_max=1.0,
                       objective="time", start=(2, 2), target=(6, 6)),
     # C1 desk: pkg/configs/desk_env.json + desk_run_*.json
-    "desk": _wl("desk", 50, 60, 500, start=(25, 12), target=(25, 38)),
+    "desk": _wl("desk", 50, 60, 500, start=(25, 12), target=(25, 38), subgrid_hint=(4, 6)),
     "desk_energy": _wl("desk_energy", 50, 60, 500, "energy", start=(25, 12), target=(25, 38)),
     "desk_net_energy": _wl("desk_net_energy", 50, 60, 500, "net_energy", start=(25, 12), target=(25, 38)),
     "desk_1k": _wl("desk_1k", 50, 60, 1000, start=(25, 12), target=(25, 38)),
     # C2 paper-scale, time objective (BASELINE.json configs[1])
-    "paper": _wl("paper", 100, 100, 5000, side=12, pos=((44, 44),), width=12.0, start=(50, 24), target=(50, 76)),
+    "paper": _wl("paper", 100, 100, 5000, side=12, pos=((44, 44),), width=12.0, start=(50, 24), target=(50, 76),
+                 subgrid_hint=(5, 5)),
     "paper_wide": _wl("paper_wide", 100, 100, 5000, amp=3.0, side=12, pos=((44, 44),), width=12.0,
                       start=(50, 24), target=(50, 76)),
     # C3 energy, C4 net-energy + two moving obstacles

@@ -246,3 +246,34 @@ def test_reference_types_accepted():
     m = fm.build_model(ctx, sub)
     om = O.build_model(env, acts, rcfg, target, sub.half_width_x, sub.half_width_y)
     assert model_digest(m) == model_digest(om)
+
+
+@pytest.mark.parametrize("case", ["random", "tiny", "smoke", "desk", "paper_1k"])
+def test_velocity_max_exact(case):
+    """k_vmax (FP32 scan + exact f64 recompute of candidates) equals the
+    oracle's exact f64 scan bit for bit (compute_subgrid's vmax)."""
+    from paper_2109_00857_b200 import workloads
+    envs = []
+    if case == "random":
+        envs = [make_random_env(s)[0] for s in RANDOM_SEEDS]
+    elif case == "tiny":
+        envs = [make_tiny_env()]
+    elif case == "paper_1k":
+        envs = [workloads.get("paper").with_(n_realizations=1000).environment()]
+    else:
+        envs = [make_named_env(case)[0]]
+    for env in envs:
+        got = DeviceEnv.from_host(env).velocity_max()
+        want = O.velocity_max(env.field)
+        assert np.float64(got[0]).tobytes() == np.float64(want[0]).tobytes()
+        assert np.float64(got[1]).tobytes() == np.float64(want[1]).tobytes()
+
+
+@pytest.mark.parametrize("name", ["desk", "paper"])
+def test_workload_subgrid_hints(name):
+    """bench.py's CPU sample uses these pinned sub-grids; the GPU's exact scan must agree."""
+    from paper_2109_00857_b200 import workloads
+    w = workloads.get(name)
+    env = w.environment()
+    sub = fm.compute_subgrid(env.field, w.actions(), env.grid)
+    assert (sub.half_width_x, sub.half_width_y) == w.subgrid_hint
