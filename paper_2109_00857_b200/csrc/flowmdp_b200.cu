@@ -13,6 +13,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <atomic>
+#include <climits>
 #include <string>
 #include <vector>
 
@@ -522,39 +523,106 @@ __device__ __forceinline__ void step_one(const BuildK &K, const BuildK *__restri
 }
 
 // u16 counters laid out [slot][lane]: one IMAD + LDS.U16 + IADD + STS.U16
-#define FM_HIST(SLOT) h16[(SLOT) * 32] += (uint16_t)1
+// The full per-transition logic (tiers of step_one with obstacle handling)
+// for the rare transitions the branch-free fast path cannot settle.
+// Returns the slot relative to the row's window origin (q = slot - soff).
+template <int FLAGS>
+__device__ __noinline__ SlowOut rare_transition(const BuildK *__restrict__ Kg, int t, const RowC R, const double2 v)
+{
+    const BuildK &K = *Kg;
+    const double *g_n = K.g + (size_t)(t + 1) * K.nc;
+    const uint8_t *mask_n = K.mask + (size_t)(t + 1) * K.nc;
+    SlowOut o;
+    o.viol = 0;
+    RowC Ra = R;   // fast-path form -> absolute target slot
+    Ra.tslot = R.tslot == INT_MIN ? -1 : R.tslot + R.soff;
+    step_one<FLAGS, true>(K, Kg, t, Ra, v, g_n, mask_n, o.slot, o.rw, o.viol);
+    o.slot -= R.soff;
+    return o;
+}
 
-// The realization loop of one chunk for the row lanes: 4 transitions per
-// iteration with their v loads hoisted, reward sums in ascending r order.
-template <int FLAGS, bool OBST>
+// Branch-free fast transition: valid when the row is plain (no dead source,
+// no obstacle within reach) and the landing is inside the row's
+// grid-clipped window (EDGE adds: or outside the domain -> SINK).
+template <int FLAGS, bool EDGE>
+__device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, const double2 v,
+                                                const double *__restrict__ g_n, int outq, int &q, double &rw)
+{
+    double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
+    if (!(FLAGS & F_DT_ONE)) {
+        px = DMUL(px, K.dt);
+        py = DMUL(py, K.dt);
+    }
+    const double x1 = DADD(R.x0, px), y1 = DADD(R.y0, py);
+    const int i1 = __double2int_rd(to_cell<FLAGS>(x1, K.ox, K.dx, K.inv_dx));
+    const int j1 = __double2int_rd(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx));
+    const bool inwin = (unsigned)(i1 - R.ilc) <= (unsigned)R.wi && (unsigned)(j1 - R.jlc) <= (unsigned)R.wj;
+    q = j1 * K.width + i1;                       // slot - soff
+    const bool hit = q == R.tslot;               // R.tslot holds tslot - soff
+    if (FLAGS & F_NET) {
+        const double gd = inwin ? __ldg(g_n + j1 * K.nx + i1) : 0.0;
+        double b = DADD(R.AB, DMUL(K.h_cr, gd));
+        if (!(FLAGS & F_DT_ONE)) b = DMUL(b, K.dt);
+        rw = hit ? DADD(b, K.r_term) : b;
+    } else {
+        rw = hit ? R.base_hit : R.base;
+    }
+    if (EDGE) {
+        const bool out = (unsigned)i1 >= (unsigned)K.nx || (unsigned)j1 >= (unsigned)K.ny;
+        if (!inwin) {
+            q = outq;
+            rw = K.r_out;
+        }
+        return R.rflags == 0 && (inwin || out);
+    }
+    return R.rflags == 0 && inwin;
+}
+
+// The realization loop of one chunk for the row lanes: 4 independent
+// transitions per iteration in straight-line code (interleaved by the
+// compiler), one warp vote to divert rare lanes, reward sums in ascending r.
+// h16q points at the row's histogram origin shifted by soff (q indexing).
+template <int FLAGS, bool EDGE>
 __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
                                            const double2 *vrow, int nk, const double *__restrict__ g_n,
-                                           const uint8_t *__restrict__ mask_n, uint16_t *h16, double &S, int &viol)
+                                           uint16_t *h16q, int outq, double &S, int &viol)
 {
     int k = 0;
     for (; k + 4 <= nk; k += 4) {
         const double2 v0 = vrow[k], v1 = vrow[k + 1], v2 = vrow[k + 2], v3 = vrow[k + 3];
-        int s0, s1, s2, s3;
+        int q0, q1, q2, q3;
         double w0, w1, w2, w3;
-        step_one<FLAGS, OBST>(K, Kg, t, R, v0, g_n, mask_n, s0, w0, viol);
-        step_one<FLAGS, OBST>(K, Kg, t, R, v1, g_n, mask_n, s1, w1, viol);
-        step_one<FLAGS, OBST>(K, Kg, t, R, v2, g_n, mask_n, s2, w2, viol);
-        step_one<FLAGS, OBST>(K, Kg, t, R, v3, g_n, mask_n, s3, w3, viol);
+        const bool f0 = fast_transition<FLAGS, EDGE>(K, R, v0, g_n, outq, q0, w0);
+        const bool f1 = fast_transition<FLAGS, EDGE>(K, R, v1, g_n, outq, q1, w1);
+        const bool f2 = fast_transition<FLAGS, EDGE>(K, R, v2, g_n, outq, q2, w2);
+        const bool f3 = fast_transition<FLAGS, EDGE>(K, R, v3, g_n, outq, q3, w3);
+        if (!__all_sync(kFull, f0 && f1 && f2 && f3)) {
+            if (!f0) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v0); q0 = o.slot; w0 = o.rw; viol |= o.viol; }
+            if (!f1) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v1); q1 = o.slot; w1 = o.rw; viol |= o.viol; }
+            if (!f2) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v2); q2 = o.slot; w2 = o.rw; viol |= o.viol; }
+            if (!f3) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v3); q3 = o.slot; w3 = o.rw; viol |= o.viol; }
+        }
         S = DADD(S, w0);   // ascending realization order (model_builder.py:457-458)
         S = DADD(S, w1);
         S = DADD(S, w2);
         S = DADD(S, w3);
-        FM_HIST(s0);
-        FM_HIST(s1);
-        FM_HIST(s2);
-        FM_HIST(s3);
+        h16q[q0 * 32] += (uint16_t)1;   // u16 counters [slot][lane]
+        h16q[q1 * 32] += (uint16_t)1;
+        h16q[q2 * 32] += (uint16_t)1;
+        h16q[q3 * 32] += (uint16_t)1;
     }
     for (; k < nk; ++k) {
-        int s0;
+        int q0;
         double w0;
-        step_one<FLAGS, OBST>(K, Kg, t, R, vrow[k], g_n, mask_n, s0, w0, viol);
+        const bool f0 = fast_transition<FLAGS, EDGE>(K, R, vrow[k], g_n, outq, q0, w0);
+        if (!f0) {
+            const SlowOut o = rare_transition<FLAGS>(Kg, t, R, vrow[k]);
+            q0 = o.slot;
+            w0 = o.rw;
+            viol |= o.viol;
+        }
         S = DADD(S, w0);
-        FM_HIST(s0);
+        h16q[q0 * 32] += (uint16_t)1;
     }
 }
 
@@ -656,6 +724,9 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
             if ((unsigned)(tci - R.ilc) <= (unsigned)R.wi && (unsigned)(tcj - R.jlc) <= (unsigned)R.wj)
                 R.tslot = tcj * W + tci + R.soff;
         }
+        // rows whose window is clipped by the domain boundary can land outside it
+        const bool edge_row = row_ok && (R.ci - K.hx < 0 || R.ci + K.hx >= K.nx || R.cj - K.hy < 0 ||
+                                         R.cj + K.hy >= K.ny);
         double S = 0.0;
         int viol = 0;
 
@@ -668,7 +739,13 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
                 h16[nslot * 32] = (uint16_t)nr;
             }
         } else {
-            const bool obst = __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
+            const bool edge = __any_sync(kFull, edge_row);
+            // fast-path form of the row constants: target slot and OUT slot in
+            // q = slot - soff coordinates, histogram pointer shifted by soff
+            RowC Rf = R;
+            Rf.tslot = R.tslot >= 0 ? R.tslot - R.soff : INT_MIN;
+            const int outq = nslot - R.soff;
+            uint16_t *h16q = h16 + R.soff * 32;
             // stage the CW cells' modes
             for (int i = lane; i < CW * nm; i += 32) {
                 const int cs = i / nm, m = i - (i / nm) * nm;
@@ -683,22 +760,27 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
             if (rec_ok) mu = *reinterpret_cast<const double2 *>(K.mean + ((size_t)t * K.nc + K.cell0 + lc_rec) * 2);
             const double *cf_t = K.coeffs + (size_t)t * nr * nm;
             const double *g_n = K.g + (size_t)(t + 1) * K.nc;
-            const uint8_t *mask_n = K.mask + (size_t)(t + 1) * K.nc;
             const double2 *vrow = vbuf + cs_row * (RC + 1);
             // chunk loader: coefficients [r0, r0+RC) x [0, nm) land transposed
             // as coefT[m][r - r0] (conflict-free reads in the reconstruction);
             // element-granular cp.async, contiguous (coalesced) global reads.
             auto issue_chunk = [&](int r0) {
                 const int n_el = min(RC, nr - r0) * nm;
-                const double *src = cf_t + (size_t)r0 * nm;
-                int er = e_r0, em = e_m0;
-                for (int i = lane; i < n_el; i += 32) {
-                    cp_async8(coefT + em * RC + er, src + i);
-                    er += e_dr;
-                    em += e_dm;
-                    if (em >= nm) {
-                        em -= nm;
-                        ++er;
+                const double *src = cf_t + (size_t)r0 * nm + lane;
+                if (e_dm == 0) {   // nm divides 32: this lane always copies mode e_m0
+                    double *dst = coefT + e_m0 * RC + e_r0;
+#pragma unroll 4
+                    for (int i = lane; i < n_el; i += 32, src += 32, dst += e_dr) cp_async8(dst, src);
+                } else {
+                    int er = e_r0, em = e_m0;
+                    for (int i = lane; i < n_el; i += 32, src += 32) {
+                        cp_async8(coefT + em * RC + er, src);
+                        er += e_dr;
+                        em += e_dm;
+                        if (em >= nm) {
+                            em -= nm;
+                            ++er;
+                        }
                     }
                 }
                 cp_async_commit();
@@ -727,10 +809,10 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
                 if (r0 + RC < nr) issue_chunk(r0 + RC);   // lands while the rows work
                 const int nk = min(RC, nr - r0);
                 if (row_ok) {
-                    if (obst)
-                        chunk_rows<FLAGS, true>(K, Kg, t, R, vrow, nk, g_n, mask_n, h16, S, viol);
+                    if (edge)
+                        chunk_rows<FLAGS, true>(K, Kg, t, Rf, vrow, nk, g_n, h16q, outq, S, viol);
                     else
-                        chunk_rows<FLAGS, false>(K, Kg, t, R, vrow, nk, g_n, mask_n, h16, S, viol);
+                        chunk_rows<FLAGS, false>(K, Kg, t, Rf, vrow, nk, g_n, h16q, outq, S, viol);
                 }
                 __syncwarp();
             }
