@@ -585,7 +585,7 @@ __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, 
 template <int FLAGS, bool EDGE>
 __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
                                            const double2 *vrow, int nk, const double *__restrict__ g_n,
-                                           uint16_t *h16q, int outq, double &S, int &viol)
+                                           uint16_t *h16q, int outq, unsigned rowmask, double &S, int &viol)
 {
     int k = 0;
     for (; k + 4 <= nk; k += 4) {
@@ -596,7 +596,7 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
         const bool f1 = fast_transition<FLAGS, EDGE>(K, R, v1, g_n, outq, q1, w1);
         const bool f2 = fast_transition<FLAGS, EDGE>(K, R, v2, g_n, outq, q2, w2);
         const bool f3 = fast_transition<FLAGS, EDGE>(K, R, v3, g_n, outq, q3, w3);
-        if (!__all_sync(kFull, f0 && f1 && f2 && f3)) {
+        if (!__all_sync(rowmask, f0 && f1 && f2 && f3)) {
             if (!f0) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v0); q0 = o.slot; w0 = o.rw; viol |= o.viol; }
             if (!f1) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v1); q1 = o.slot; w1 = o.rw; viol |= o.viol; }
             if (!f2) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v2); q2 = o.slot; w2 = o.rw; viol |= o.viol; }
@@ -740,6 +740,7 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
             }
         } else {
             const bool edge = __any_sync(kFull, edge_row);
+            const unsigned rowmask = __ballot_sync(kFull, row_ok);   // lanes that run chunk_rows
             // fast-path form of the row constants: target slot and OUT slot in
             // q = slot - soff coordinates, histogram pointer shifted by soff
             RowC Rf = R;
@@ -810,9 +811,9 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
                 const int nk = min(RC, nr - r0);
                 if (row_ok) {
                     if (edge)
-                        chunk_rows<FLAGS, true>(K, Kg, t, Rf, vrow, nk, g_n, h16q, outq, S, viol);
+                        chunk_rows<FLAGS, true>(K, Kg, t, Rf, vrow, nk, g_n, h16q, outq, rowmask, S, viol);
                     else
-                        chunk_rows<FLAGS, false>(K, Kg, t, Rf, vrow, nk, g_n, h16q, outq, S, viol);
+                        chunk_rows<FLAGS, false>(K, Kg, t, Rf, vrow, nk, g_n, h16q, outq, rowmask, S, viol);
                 }
                 __syncwarp();
             }
