@@ -335,7 +335,7 @@ struct BuildK {
     int CW, RW, AG, nag, groups, RC;
     long long n_tasks;
     // per-warp shared-memory carve-up (bytes)
-    int smem_warp, off_vbuf, off_coef, off_modes;
+    int smem_warp, off_vbuf, off_coef, off_modes, off_danger;
     // outputs
     uint64_t *row_ptr;
     uint16_t *row_nnz;
@@ -541,12 +541,15 @@ __device__ __noinline__ SlowOut rare_transition(const BuildK *__restrict__ Kg, i
     return o;
 }
 
-// Branch-free fast transition: valid when the row is plain (no dead source,
-// no obstacle within reach) and the landing is inside the row's
-// grid-clipped window (EDGE adds: or outside the domain -> SINK).
-template <int FLAGS, bool EDGE>
+// Branch-free fast transition.  Valid when the landing is inside the row's
+// grid-clipped window and (OBST) not on a danger slot of the row's cell --
+// a cell masked at t+1 or a gated segment whose box touches the mask at t --
+// or (EDGE) outside the domain (-> SINK).  Dead source rows (OBST) are
+// overridden here; everything else goes to rare_transition.
+template <int FLAGS, bool EDGE, bool OBST>
 __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, const double2 v,
-                                                const double *__restrict__ g_n, int outq, int &q, double &rw)
+                                                const double *__restrict__ g_n, const uint32_t *dang, int outq,
+                                                int &q, double &rw)
 {
     double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
     if (!(FLAGS & F_DT_ONE)) {
@@ -567,35 +570,47 @@ __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, 
     } else {
         rw = hit ? R.base_hit : R.base;
     }
+    bool ok = inwin;
+    if (OBST) {
+        const int slot = q + R.soff;
+        const bool dz = inwin && ((dang[slot >> 5] >> (slot & 31)) & 1u);
+        const bool dead = R.rflags & RF_DEAD;
+        ok = inwin && (!dz || dead);
+        if (dead) {   // after the overflow check (model_builder.py:445-452)
+            q = outq;
+            rw = (R.rflags & RF_TERMINAL) ? 0.0 : K.r_out;
+        }
+    }
     if (EDGE) {
         const bool out = (unsigned)i1 >= (unsigned)K.nx || (unsigned)j1 >= (unsigned)K.ny;
         if (!inwin) {
             q = outq;
-            rw = K.r_out;
+            rw = (OBST && (R.rflags & RF_TERMINAL)) ? 0.0 : K.r_out;
         }
-        return R.rflags == 0 && (inwin || out);
+        ok = ok || out;
     }
-    return R.rflags == 0 && inwin;
+    return ok;
 }
 
 // The realization loop of one chunk for the row lanes: 4 independent
 // transitions per iteration in straight-line code (interleaved by the
 // compiler), one warp vote to divert rare lanes, reward sums in ascending r.
 // h16q points at the row's histogram origin shifted by soff (q indexing).
-template <int FLAGS, bool EDGE>
+template <int FLAGS, bool EDGE, bool OBST>
 __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
                                            const double2 *vrow, int nk, const double *__restrict__ g_n,
-                                           uint16_t *h16q, int outq, unsigned rowmask, double &S, int &viol)
+                                           const uint32_t *dang, uint16_t *h16q, int outq, unsigned rowmask,
+                                           double &S, int &viol)
 {
     int k = 0;
     for (; k + 4 <= nk; k += 4) {
         const double2 v0 = vrow[k], v1 = vrow[k + 1], v2 = vrow[k + 2], v3 = vrow[k + 3];
         int q0, q1, q2, q3;
         double w0, w1, w2, w3;
-        const bool f0 = fast_transition<FLAGS, EDGE>(K, R, v0, g_n, outq, q0, w0);
-        const bool f1 = fast_transition<FLAGS, EDGE>(K, R, v1, g_n, outq, q1, w1);
-        const bool f2 = fast_transition<FLAGS, EDGE>(K, R, v2, g_n, outq, q2, w2);
-        const bool f3 = fast_transition<FLAGS, EDGE>(K, R, v3, g_n, outq, q3, w3);
+        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, v0, g_n, dang, outq, q0, w0);
+        const bool f1 = fast_transition<FLAGS, EDGE, OBST>(K, R, v1, g_n, dang, outq, q1, w1);
+        const bool f2 = fast_transition<FLAGS, EDGE, OBST>(K, R, v2, g_n, dang, outq, q2, w2);
+        const bool f3 = fast_transition<FLAGS, EDGE, OBST>(K, R, v3, g_n, dang, outq, q3, w3);
         if (!__all_sync(rowmask, f0 && f1 && f2 && f3)) {
             if (!f0) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v0); q0 = o.slot; w0 = o.rw; viol |= o.viol; }
             if (!f1) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v1); q1 = o.slot; w1 = o.rw; viol |= o.viol; }
@@ -614,7 +629,7 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
     for (; k < nk; ++k) {
         int q0;
         double w0;
-        const bool f0 = fast_transition<FLAGS, EDGE>(K, R, vrow[k], g_n, outq, q0, w0);
+        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, vrow[k], g_n, dang, outq, q0, w0);
         if (!f0) {
             const SlowOut o = rare_transition<FLAGS>(Kg, t, R, vrow[k]);
             q0 = o.slot;
@@ -649,6 +664,7 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
     double2 *vbuf = reinterpret_cast<double2 *>(wbase + K.off_vbuf);       // [CW][RC+1]
     double *coefT = reinterpret_cast<double *>(wbase + K.off_coef);        // [nm][RC]
     double2 *modes_s = reinterpret_cast<double2 *>(wbase + K.off_modes);   // [CW][nm]
+    uint32_t *danger = reinterpret_cast<uint32_t *>(wbase + K.off_danger);  // [CW][ceil(nslot/32)]
 
     for (int sl = 0; sl <= K.nslot; ++sl) h16[sl * 32] = 0;
 
@@ -741,6 +757,31 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
         } else {
             const bool edge = __any_sync(kFull, edge_row);
             const unsigned rowmask = __ballot_sync(kFull, row_ok);   // lanes that run chunk_rows
+            const bool obst = __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
+            const int DW = (nslot + 31) >> 5;
+            if (obst) {
+                // danger[cs][slot]: landing cell masked at t+1, or (gated cell)
+                // the segment box [min(c,l)-1, max(c,l)+1] touches the mask at t
+                for (int wd = 0; wd < CW * DW; ++wd) {
+                    const int cs = wd / DW, sl = (wd - cs * DW) * 32 + lane;
+                    const int lc = grp * CW + cs;
+                    bool bit = false;
+                    if (lc < K.ncell && sl < nslot) {
+                        const int cc = K.cell0 + lc, cci = cc % K.nx, ccj = cc / K.nx;
+                        const int li = cci + sl % W - K.hx, lj = ccj + sl / W - K.hy;
+                        if ((unsigned)li < (unsigned)K.nx && (unsigned)lj < (unsigned)K.ny) {
+                            bit = K.mask[(size_t)(t + 1) * K.nc + lj * K.nx + li] != 0;
+                            if (!bit && box_count(K, t, cci - K.rx, cci + K.rx, ccj - K.ry, ccj + K.ry) > 0)
+                                bit = box_count(K, t, min(cci, li) - 1, max(cci, li) + 1, min(ccj, lj) - 1,
+                                                max(ccj, lj) + 1) > 0;
+                        }
+                    }
+                    const unsigned word = __ballot_sync(kFull, bit);
+                    if (lane == 0) danger[wd] = word;
+                }
+                __syncwarp();
+            }
+            const uint32_t *dang = danger + cs_row * DW;
             // fast-path form of the row constants: target slot and OUT slot in
             // q = slot - soff coordinates, histogram pointer shifted by soff
             RowC Rf = R;
@@ -810,10 +851,21 @@ __global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *
                 if (r0 + RC < nr) issue_chunk(r0 + RC);   // lands while the rows work
                 const int nk = min(RC, nr - r0);
                 if (row_ok) {
-                    if (edge)
-                        chunk_rows<FLAGS, true>(K, Kg, t, Rf, vrow, nk, g_n, h16q, outq, rowmask, S, viol);
-                    else
-                        chunk_rows<FLAGS, false>(K, Kg, t, Rf, vrow, nk, g_n, h16q, outq, rowmask, S, viol);
+                    if (obst) {
+                        if (edge)
+                            chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
+                                                          viol);
+                        else
+                            chunk_rows<FLAGS, false, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
+                                                           viol);
+                    } else {
+                        if (edge)
+                            chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
+                                                           viol);
+                        else
+                            chunk_rows<FLAGS, false, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask,
+                                                            S, viol);
+                    }
                 }
                 __syncwarp();
             }
@@ -981,7 +1033,8 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
     K.off_vbuf = align16((int)(nslot + 1) * 64);
     K.off_coef = K.off_vbuf + K.CW * (K.RC + 1) * (int)sizeof(double2);
     K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
-    K.smem_warp = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
+    K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
+    K.smem_warp = align16(K.off_danger + K.CW * (int)((nslot + 31) / 32) * 4);
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
     K.entries = M->entries; K.capacity = M->capacity;
     K.nnz_counter = reinterpret_cast<unsigned long long *>(M->d_nnz);
