@@ -15,7 +15,7 @@ from .errors import ContractViolation, NativeUnavailable
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libflowmdp_b200.so")
+LIB_PATH = os.environ.get("FM_LIB_PATH") or os.path.join(PKG_DIR, "libflowmdp_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 SOURCES = [os.path.join(CSRC, "flowmdp_b200.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "fm_hypot.cuh"), os.path.join(REPO_DIR, "include", "flowmdp_b200.h")]

@@ -654,7 +654,13 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
 //                      next chunk stream in with cp.async while the row lanes
 //                      work on the current one.
 template <int FLAGS>
-__global__ void __launch_bounds__(128, 4) k_build(const BuildK K, const BuildK *__restrict__ Kg)
+#ifndef FM_BUILD_MINB
+#define FM_BUILD_MINB 4
+#endif
+#ifndef FM_BUILD_RC
+#define FM_BUILD_RC 64
+#endif
+__global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, const BuildK *__restrict__ Kg)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1027,7 +1033,7 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
     K.n_tasks = (long long)(h->t1 - h->t0) * K.groups * K.nag;
     if (K.n_tasks > 0xFFFFFFF0LL) return fm_fail(FM_BAD_ARG, "fm_build: too many tasks");
     // realizations per chunk: RW recon lanes per cell, 64 realizations
-    K.RC = K.RW >= 64 ? K.RW : 64;
+    K.RC = K.RW >= FM_BUILD_RC ? K.RW : FM_BUILD_RC;
     // per-warp shared memory: u16 histogram [nslot+1][32] | v chunk [CW][RC+1]
     // | transposed coefficients [nm][RC] | modes [CW][nm]
     K.off_vbuf = align16((int)(nslot + 1) * 64);
