@@ -621,19 +621,10 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
         S = DADD(S, w1);
         S = DADD(S, w2);
         S = DADD(S, w3);
-        // u16 counters [slot][lane]: the four read-modify-writes are made
-        // independent -- each slot gets its multiplicity within the group and
-        // duplicate slots store the same final value
-        {
-            uint16_t *p0 = h16q + q0 * 32, *p1 = h16q + q1 * 32, *p2 = h16q + q2 * 32, *p3 = h16q + q3 * 32;
-            const unsigned o0 = *p0, o1 = *p1, o2 = *p2, o3 = *p3;
-            const unsigned e01 = q0 == q1, e02 = q0 == q2, e03 = q0 == q3;
-            const unsigned e12 = q1 == q2, e13 = q1 == q3, e23 = q2 == q3;
-            *p0 = (uint16_t)(o0 + 1u + e01 + e02 + e03);
-            *p1 = (uint16_t)(o1 + 1u + e01 + e12 + e13);
-            *p2 = (uint16_t)(o2 + 1u + e02 + e12 + e23);
-            *p3 = (uint16_t)(o3 + 1u + e03 + e13 + e23);
-        }
+        h16q[q0 * 32] += (uint16_t)1;   // u16 counters [slot][lane]
+        h16q[q1 * 32] += (uint16_t)1;
+        h16q[q2 * 32] += (uint16_t)1;
+        h16q[q3 * 32] += (uint16_t)1;
     }
     for (; k < nk; ++k) {
         int q0;
