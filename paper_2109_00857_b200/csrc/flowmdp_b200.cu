@@ -452,6 +452,11 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src)
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -807,19 +812,26 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
             double2 mu = make_double2(0.0, 0.0);
             if (rec_ok) mu = *reinterpret_cast<const double2 *>(K.mean + ((size_t)t * K.nc + K.cell0 + lc_rec) * 2);
             const double *cf_t = K.coeffs + (size_t)t * nr * nm;
+            // even mode count and 16-byte aligned coefficient rows: pair layout
+            const bool pairs = (nm & 1) == 0 && nm > 0 && ((reinterpret_cast<uintptr_t>(cf_t) & 15) == 0);
             const double *g_n = K.g + (size_t)(t + 1) * K.nc;
             const double2 *vrow = vbuf + cs_row * (RC + 1);
             // chunk loader: coefficients [r0, r0+RC) x [0, nm) land transposed
             // as coefT[m][r - r0] (conflict-free reads in the reconstruction);
             // element-granular cp.async, contiguous (coalesced) global reads.
             auto issue_chunk = [&](int r0) {
-                const int n_el = min(RC, nr - r0) * nm;
-                const double *src = cf_t + (size_t)r0 * nm + lane;
-                if (e_dm == 0) {   // nm divides 32: this lane always copies mode e_m0
-                    double *dst = coefT + e_m0 * RC + e_r0;
-#pragma unroll 4
-                    for (int i = lane; i < n_el; i += 32, src += 32, dst += e_dr) cp_async8(dst, src);
+                const int nrc = min(RC, nr - r0);
+                const double *src = cf_t + (size_t)r0 * nm;
+                if (pairs) {
+                    // 16-byte copies: (realization rl, modes 2p..2p+1) -> coef2[p][rl]
+                    const int np = nm >> 1, n_el = nrc * np;
+                    for (int i = lane; i < n_el; i += 32) {
+                        const int rl = i / np, pp = i - rl * np;
+                        cp_async16(coefT + ((size_t)pp * RC + rl) * 2, src + (size_t)rl * nm + 2 * pp);
+                    }
                 } else {
+                    const int n_el = nrc * nm;
+                    src += lane;
                     int er = e_r0, em = e_m0;
                     for (int i = lane; i < n_el; i += 32, src += 32) {
                         cp_async8(coefT + em * RC + er, src);
@@ -843,11 +855,23 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
                         const int rl = p * RW + rr;
                         if (r0 + rl < nr) {
                             double vx = mu.x, vy = mu.y;
-                            for (int m = 0; m < nm; ++m) {   // environment.py:295-297, ascending m
-                                const double k = coefT[m * RC + rl];
-                                const double2 mm = md[m];
-                                vx = DADD(vx, DMUL(k, mm.x));
-                                vy = DADD(vy, DMUL(k, mm.y));
+                            if (pairs) {
+                                const double2 *c2 = reinterpret_cast<const double2 *>(coefT) + rl;
+                                for (int m = 0; m < nm; m += 2) {   // environment.py:295-297, ascending m
+                                    const double2 kk = c2[(m >> 1) * RC];
+                                    const double2 ma = md[m], mb = md[m + 1];
+                                    vx = DADD(vx, DMUL(kk.x, ma.x));
+                                    vy = DADD(vy, DMUL(kk.x, ma.y));
+                                    vx = DADD(vx, DMUL(kk.y, mb.x));
+                                    vy = DADD(vy, DMUL(kk.y, mb.y));
+                                }
+                            } else {
+                                for (int m = 0; m < nm; ++m) {   // environment.py:295-297, ascending m
+                                    const double k = coefT[m * RC + rl];
+                                    const double2 mm = md[m];
+                                    vx = DADD(vx, DMUL(k, mm.x));
+                                    vy = DADD(vy, DMUL(k, mm.y));
+                                }
                             }
                             vbuf[cs_rec * (RC + 1) + rl] = make_double2(vx, vy);
                         }
