@@ -110,6 +110,8 @@ typedef struct {
     int32_t t0, t1, j0, j1;
     uint32_t *viol_flags;     /* device [nt*n_actions], zeroed by caller     */
     uint32_t *task_counter;   /* device [1] scratch, zeroed by fm_build      */
+    const int32_t *d_gate_r;  /* device [rx, ry] from fm_gate_radius, or NULL
+                                 to use rx/ry above                          */
 } fm_build_args;
 
 /* Sub-grid overflow report (message of model_builder.py:433-438). */
@@ -150,6 +152,21 @@ int32_t fm_mask_sat(const uint8_t *mask, int32_t nt, int32_t ny, int32_t nx,
  * FM_SUBGRID_OVERFLOW fills *h_viol like the reference's ContractViolation. */
 int32_t fm_build(const fm_build_args *h_args, fm_model *h_model,
                  uint64_t *h_needed, fm_violation *h_viol, void *stream);
+/* fm_build = fm_build_launch (asynchronous) + fm_build_check (synchronous:
+ * census, capacity and overflow report).  Work that consumes the model
+ * (e.g. fm_solve_backward, which never reads past `capacity`) may be queued
+ * between the two; its results are valid only if the check returns FM_OK. */
+int32_t fm_build_launch(const fm_build_args *h_args, fm_model *h_model, void *stream);
+int32_t fm_build_check(const fm_build_args *h_args, fm_model *h_model,
+                       uint64_t *h_needed, fm_violation *h_viol, void *stream);
+
+/* Obstacle-gate radius without a host round trip (model_builder.py:218-223,
+ * environment.py:404-419): inputs are the fm_maxabs_segments results
+ * max|mean| [nt][2], max|coeff| [nt][n_modes], max|mode| [n_modes][nt][2];
+ * d_out2 = (rx, ry), d_bound2 (optional) = velocity_bound. */
+int32_t fm_gate_radius(fm_grid grid, const double *meanmax, const double *coefmax,
+                       const double *modemax, int32_t n_modes, double f_max,
+                       int32_t *d_out2, double *d_bound2, void *stream);
 
 /* Export to the reference's canonical COO blocks, SparseModel layout
  * (model_builder.py:157-178, 474-501, 568-573): blocks in [a][t] order,

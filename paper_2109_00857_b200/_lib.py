@@ -90,7 +90,7 @@ class FmBuildArgs(C.Structure):
                 ("hx", C.c_int32), ("hy", C.c_int32), ("rx", C.c_int32), ("ry", C.c_int32),
                 ("mask_sat", C.c_void_p),
                 ("t0", C.c_int32), ("t1", C.c_int32), ("j0", C.c_int32), ("j1", C.c_int32),
-                ("viol_flags", C.c_void_p), ("task_counter", C.c_void_p)]
+                ("viol_flags", C.c_void_p), ("task_counter", C.c_void_p), ("d_gate_r", C.c_void_p)]
 
 
 class FmViolation(C.Structure):
@@ -114,6 +114,11 @@ SIGNATURES = {
     "fm_mask_sat": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "fm_build": (C.c_int32, [C.POINTER(FmBuildArgs), C.POINTER(FmModel), C.POINTER(C.c_uint64),
                              C.POINTER(FmViolation), C.c_void_p]),
+    "fm_build_launch": (C.c_int32, [C.POINTER(FmBuildArgs), C.POINTER(FmModel), C.c_void_p]),
+    "fm_build_check": (C.c_int32, [C.POINTER(FmBuildArgs), C.POINTER(FmModel), C.POINTER(C.c_uint64),
+                                   C.POINTER(FmViolation), C.c_void_p]),
+    "fm_gate_radius": (C.c_int32, [FmGrid, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_double,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "fm_export_coo": (C.c_int32, [C.POINTER(FmModel), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "fm_solve_backward": (C.c_int32, [C.POINTER(FmModel), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,

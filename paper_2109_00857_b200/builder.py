@@ -99,6 +99,11 @@ class DeviceEnv:
                           self.g.data_ptr(), self.mask.data_ptr(), self.n_modes, self.n_real)
 
     # -- velocity statistics ------------------------------------------------
+    def reset_derived(self):
+        """Forget cached sub-grid / gate statistics (they are recomputed)."""
+        self._vmax = None
+        self._vbound = {}
+
     def velocity_max(self) -> tuple:
         """Exact max |v_x|, |v_y| over (t, r, cell) -- compute_subgrid's scan."""
         if self._vmax is None:
@@ -110,10 +115,10 @@ class DeviceEnv:
             self._vmax = (float(h[0]), float(h[1]))
         return self._vmax
 
-    def velocity_bound(self) -> tuple:
-        """Triangle bound of environment.py:404-419: device max-abs
-        reductions, then the reference's per-t combination on the host."""
-        if "b" not in self._vbound:
+    def _maxima(self):
+        """Device max-abs reductions behind velocity_bound (environment.py:404-419):
+        max|mean| [nt][2], max|coeff| [nt][n_modes], max|mode| [n_modes][nt][2]."""
+        if "mx" not in self._vbound:
             torch = _torch()
             g, nm, nr = self.grid, self.n_modes, self.n_real
             nc = g.nx * g.ny
@@ -130,6 +135,28 @@ class DeviceEnv:
                                                 coef_mx.data_ptr(), s), "maxabs coeffs")
                 _lib.check(L.fm_maxabs_segments(self.modes.data_ptr(), nm * g.nt * 2, nc, 2, 2, nc * 2, 1,
                                                 mode_mx.data_ptr(), s), "maxabs modes")
+            self._vbound["mx"] = (mean_mx, coef_mx, mode_mx)
+        return self._vbound["mx"]
+
+    def gate_radius_device(self, f_max: float):
+        """(rx, ry) of the obstacle gate as a device int32[2], no host round trip."""
+        key = ("gate", float(f_max))
+        if key not in self._vbound:
+            torch = _torch()
+            mean_mx, coef_mx, mode_mx = self._maxima()
+            out = torch.empty(2, dtype=torch.int32, device=self.mean.device)
+            _lib.check(_lib.load().fm_gate_radius(self.fm_grid(), mean_mx.data_ptr(), coef_mx.data_ptr(),
+                                                  mode_mx.data_ptr(), self.n_modes, float(f_max), out.data_ptr(),
+                                                  None, _lib.stream_ptr()), "fm_gate_radius")
+            self._vbound[key] = out
+        return self._vbound[key]
+
+    def velocity_bound(self) -> tuple:
+        """Triangle bound of environment.py:404-419: device max-abs
+        reductions, then the reference's per-t combination on the host."""
+        if "b" not in self._vbound:
+            g, nm = self.grid, self.n_modes
+            mean_mx, coef_mx, mode_mx = self._maxima()
             mean_mx = mean_mx.cpu().numpy().reshape(g.nt, 2)
             coef_mx = coef_mx.cpu().numpy()[: g.nt * nm].reshape(g.nt, nm)
             mode_mx = mode_mx.cpu().numpy()[: nm * g.nt * 2].reshape(nm, g.nt, 2)
@@ -234,6 +261,38 @@ class DeviceModel:
     def n_states(self) -> int:
         return self.grid.nt * self.grid.nx * self.grid.ny + 1
 
+    _pending: tuple | None = None
+
+    def check(self) -> bool:
+        """Finish a (deferred) build: census, sub-grid overflow (raises the
+        reference's ContractViolation), capacity.  Returns True if the model
+        had to be rebuilt with a larger entry buffer (consumers queued after
+        the launch must then be re-run)."""
+        if self._pending is None:
+            return False
+        args, keep = self._pending
+        L = _lib.load()
+        rebuilt = False
+        for _attempt in range(2):
+            m = self.fm_model()
+            needed = C.c_uint64(0)
+            vio = _lib.FmViolation()
+            st = L.fm_build_check(C.byref(args), C.byref(m), C.byref(needed), C.byref(vio), _lib.stream_ptr())
+            if st == _lib.FM_CAPACITY:
+                torch = _torch()
+                self.entries = torch.empty(int(needed.value) + 1024, dtype=torch.int32, device=self.entries.device)
+                self.d_nnz.zero_()
+                keep[2].zero_()
+                m = self.fm_model()
+                _lib.check(L.fm_build_launch(C.byref(args), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
+                rebuilt = True
+                continue
+            _lib.check(st, "fm_build")
+            self.nnz = int(needed.value)
+            self._pending = None
+            return rebuilt
+        raise RuntimeError("fm_build: capacity retry failed")
+
     def fm_model(self) -> _lib.FmModel:
         g = self.grid
         return _lib.FmModel(g.nx, g.ny, g.nt, self.n_actions, self.n_real,
@@ -282,8 +341,13 @@ class DeviceModel:
 
 def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridSpec,
                        t_range: tuple | None = None, j_range: tuple | None = None,
-                       capacity_hint: int | None = None) -> DeviceModel:
-    """Run K_build over slabs t_range x row strip j_range; model stays in HBM."""
+                       capacity_hint: int | None = None, defer_check: bool = False) -> DeviceModel:
+    """Run K_build over slabs t_range x row strip j_range; the model stays in HBM.
+
+    With defer_check the kernel is only enqueued: consumers (the backward
+    solve) can be queued behind it and ``DeviceModel.check()`` performs the
+    census / overflow / capacity check later (it rebuilds on a capacity
+    miss and returns True when it did)."""
     torch = _torch()
     L = _lib.load()
     grid = denv.grid
@@ -292,46 +356,40 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
         raise ContractViolation(f"target cell {tuple(target)} outside grid")
     t0, t1 = t_range if t_range is not None else (0, grid.nt)
     j0, j1 = j_range if j_range is not None else (0, grid.ny)
+    full = (t0, t1) == (0, grid.nt) and (j0, j1) == (0, grid.ny)
     dev = denv.mean.device
     recs = action_records(actions, rcfg, grid)
     na = recs.shape[0]
-    d_act = torch.from_numpy(recs).to(dev)
-    rx, ry = gate_radius(denv, float(actions.f_max))
+    d_act = torch.from_numpy(recs).pin_memory().to(dev, non_blocking=True)
+    d_gate = denv.gate_radius_device(float(actions.f_max))
     hx, hy = subgrid.half_width_x, subgrid.half_width_y
     nc = grid.nx * grid.ny
     n_rows = grid.nt * nc * na
     active_rows = (t1 - t0) * (j1 - j0) * grid.nx * na
     n_slot1 = (2 * hx + 1) * (2 * hy + 1) + 1
     cap = capacity_hint if capacity_hint else active_rows * min(n_slot1, denv.n_real, 6) + 1024
-
+    alloc = torch.empty if full else torch.zeros
     row_ptr = torch.empty(n_rows, dtype=torch.int64, device=dev)
-    row_nnz = torch.zeros(n_rows, dtype=torch.int16, device=dev)
-    reward = torch.zeros(n_rows, dtype=torch.float64, device=dev)
+    row_nnz = alloc(n_rows, dtype=torch.int16, device=dev)
+    reward = alloc(n_rows, dtype=torch.float64, device=dev)
     d_nnz = torch.zeros(1, dtype=torch.int64, device=dev)
     viol = torch.zeros(grid.nt * na, dtype=torch.int32, device=dev)
     counter = torch.zeros(1, dtype=torch.int32, device=dev)
     rw = _lib.FmReward(OBJECTIVE_CODE[rcfg.objective], float(rcfg.c_f), float(rcfg.c_r),
                        float(rcfg.r_term), float(rcfg.r_outbound), ti, tj)
-    args = _lib.FmBuildArgs(denv.fm_grid(), denv.fm_env(), rw, d_act.data_ptr(), na, hx, hy, rx, ry,
-                            denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr())
-    for _attempt in range(2):
-        entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
-        dm = DeviceModel(grid=grid, n_actions=na, n_real=denv.n_real, subgrid=subgrid,
-                         row_ptr=row_ptr, row_nnz=row_nnz, reward=reward, entries=entries,
-                         d_nnz=d_nnz, nnz=0, t_range=(t0, t1), j_range=(j0, j1))
-        m = dm.fm_model()
-        needed = C.c_uint64(0)
-        vio = _lib.FmViolation()
-        st = L.fm_build(C.byref(args), C.byref(m), C.byref(needed), C.byref(vio), _lib.stream_ptr())
-        if st == _lib.FM_CAPACITY:
-            cap = int(needed.value) + 1024
-            d_nnz.zero_()
-            viol.zero_()
-            continue
-        _lib.check(st, "fm_build")
-        dm.nnz = int(needed.value)
-        return dm
-    raise RuntimeError("fm_build: capacity retry failed")
+    args = _lib.FmBuildArgs(denv.fm_grid(), denv.fm_env(), rw, d_act.data_ptr(), na, hx, hy, 0, 0,
+                            denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr(),
+                            d_gate.data_ptr())
+    entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
+    dm = DeviceModel(grid=grid, n_actions=na, n_real=denv.n_real, subgrid=subgrid,
+                     row_ptr=row_ptr, row_nnz=row_nnz, reward=reward, entries=entries,
+                     d_nnz=d_nnz, nnz=0, t_range=(t0, t1), j_range=(j0, j1))
+    dm._pending = (args, (d_act, d_gate, viol, counter, denv))
+    m = dm.fm_model()
+    _lib.check(L.fm_build_launch(C.byref(args), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
+    if not defer_check:
+        dm.check()
+    return dm
 
 
 def build_model(ctx, subgrid: SubGridSpec, n_threads: int = 1) -> SparseModel:

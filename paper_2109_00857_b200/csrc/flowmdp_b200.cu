@@ -330,6 +330,7 @@ struct BuildK {
     // sub-grid
     int hx, hy, width, nslot, hw;
     int rx, ry;
+    const int32_t *gate_r;   // device [rx, ry] (fm_gate_radius) or null
     // task decomposition
     int t0, t1, cell0, ncell;   // strip = cells [cell0, cell0 + ncell) of each layer
     int CW, RW, AG, nag, groups, RC;
@@ -705,6 +706,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
         const bool row_ok = row_lane && lc_row < K.ncell && a < K.na;
         const int c = K.cell0 + lc_row;
         const bool horizon = (t + 1 >= K.nt);
+        const int rx = K.gate_r ? __ldg(K.gate_r) : K.rx, ry = K.gate_r ? __ldg(K.gate_r + 1) : K.ry;
 
         // ---- per-row constants
         RowC R;
@@ -730,7 +732,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
             if (terminal) R.rflags |= RF_TERMINAL;
             if (!horizon) {
                 // the reference's obstacle gate (model_builder.py:218-228, 339-345)
-                if (box_count(K, t, ci - K.rx, ci + K.rx, cj - K.ry, cj + K.ry) > 0) {
+                if (box_count(K, t, ci - rx, ci + rx, cj - ry, cj + ry) > 0) {
                     R.rflags |= RF_GATE;
                     // an in-window segment only touches cells within one of the window
                     if (box_count(K, t, ci - K.hx - 1, ci + K.hx + 1, cj - K.hy - 1, cj + K.hy + 1) > 0)
@@ -782,7 +784,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
                         const int li = cci + sl % W - K.hx, lj = ccj + sl / W - K.hy;
                         if ((unsigned)li < (unsigned)K.nx && (unsigned)lj < (unsigned)K.ny) {
                             bit = K.mask[(size_t)(t + 1) * K.nc + lj * K.nx + li] != 0;
-                            if (!bit && box_count(K, t, cci - K.rx, cci + K.rx, ccj - K.ry, ccj + K.ry) > 0)
+                            if (!bit && box_count(K, t, cci - rx, cci + rx, ccj - ry, ccj + ry) > 0)
                                 bit = box_count(K, t, min(cci, li) - 1, max(cci, li) + 1, min(ccj, lj) - 1,
                                                 max(ccj, lj) + 1) > 0;
                         }
@@ -962,7 +964,8 @@ __global__ void k_viol_report(const BuildK *__restrict__ Kg, int t, int a, int p
     const bool inb = (unsigned)i1 < (unsigned)K.nx && (unsigned)j1 < (unsigned)K.ny;
     bool bad = !inb;
     if (inb) bad = K.mask[(size_t)(t + 1) * K.nc + j1 * K.nx + i1] != 0;
-    if (!bad && box_count(K, t, ci - K.rx, ci + K.rx, cj - K.ry, cj + K.ry) > 0)
+    const int rx = K.gate_r ? K.gate_r[0] : K.rx, ry = K.gate_r ? K.gate_r[1] : K.ry;
+    if (!bad && box_count(K, t, ci - rx, ci + rx, cj - ry, cj + ry) > 0)
         bad = seg_blocked<0>(K, t, x0, y0, x1, y1);
     if (bad) return;
     const int di = i1 - ci, dj = j1 - cj;
@@ -1012,10 +1015,9 @@ static bool is_pow2(double x)
 
 static int align16(int x) { return (x + 15) & ~15; }
 
-extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_needed, fm_violation *h_viol,
-                            void *stream)
+// validates the arguments and fills the kernel parameter block + flags
+static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K, int &flags)
 {
-    cudaStream_t s = (cudaStream_t)stream;
     const fm_grid &G = h->grid;
     if (G.nx < 1 || G.ny < 1 || G.nt < 1 || !(G.dx > 0) || !(G.dt > 0))
         return fm_fail(FM_BAD_ARG, "fm_build: bad grid");
@@ -1032,7 +1034,6 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
     if (h->reward.target_i < 0 || h->reward.target_i >= G.nx || h->reward.target_j < 0 || h->reward.target_j >= G.ny)
         return fm_fail(FM_BAD_ARG, "target cell (%d, %d) outside grid", h->reward.target_i, h->reward.target_j);
 
-    BuildK K;
     K.nx = G.nx; K.ny = G.ny; K.nt = G.nt; K.nc = G.nx * G.ny;
     K.dx = G.dx; K.dt = G.dt; K.ox = G.ox; K.oy = G.oy;
     K.inv_dx = 1.0 / G.dx;
@@ -1070,21 +1071,43 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
     K.nnz_counter = reinterpret_cast<unsigned long long *>(M->d_nnz);
     K.viol = h->viol_flags; K.task_counter = h->task_counter;
 
-    int flags = 0;
+    flags = 0;
     if (G.dt == 1.0) flags |= F_DT_ONE;
     if (G.ox == 0.0 && G.oy == 0.0) flags |= F_OX_ZERO;
     if (G.dx == 1.0) flags |= F_DX_ONE;
     else if (is_pow2(G.dx)) flags |= F_DX_MUL;
     if (K.obj == FM_OBJ_NET_ENERGY) flags |= F_NET;
 
+    K.gate_r = h->d_gate_r;
+    return FM_OK;
+}
+
+extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    BuildK K;
+    int flags = 0;
+    int32_t st = build_params(h, M, K, flags);
+    if (st != FM_OK) return st;
     BuildK *Kg = nullptr;
     FM_CK(cudaMallocAsync(&Kg, sizeof(BuildK), s));
     FM_CK(cudaMemcpyAsync(Kg, &K, sizeof(BuildK), cudaMemcpyHostToDevice, s));
     FM_CK(cudaMemsetAsync(h->task_counter, 0, sizeof(unsigned int), s));
-    const size_t smem = (size_t)4 * K.smem_warp;
-    int32_t st = launch_build(K, Kg, flags, smem, s);
+    st = launch_build(K, Kg, flags, (size_t)4 * K.smem_warp, s);
     if (st != FM_OK) return st;
+    FM_CK(cudaFreeAsync(Kg, s));
+    return FM_OK;
+}
 
+extern "C" int32_t fm_build_check(const fm_build_args *h, fm_model *M, uint64_t *h_needed, fm_violation *h_viol,
+                                  void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    BuildK K;
+    int flags = 0;
+    int32_t st = build_params(h, M, K, flags);
+    if (st != FM_OK) return st;
+    const fm_grid &G = h->grid;
     // census + violation flags back to the host (the reference raises
     // before returning anything, so the error check is synchronous).
     unsigned long long nnz = 0;
@@ -1096,7 +1119,10 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
         for (int a = 0; a < h->n_actions; ++a) {
             if (!flags_h[(size_t)t * h->n_actions + a]) continue;
             // reproduce the reference message for the first (t, a)
+            BuildK *Kg = nullptr;
             unsigned long long *d_best;
+            FM_CK(cudaMallocAsync(&Kg, sizeof(BuildK), s));
+            FM_CK(cudaMemcpyAsync(Kg, &K, sizeof(BuildK), cudaMemcpyHostToDevice, s));
             FM_CK(cudaMallocAsync(&d_best, sizeof(unsigned long long) + 2 * sizeof(int32_t), s));
             int32_t *d_didj = reinterpret_cast<int32_t *>(d_best + 1);
             FM_CK(cudaMemsetAsync(d_best, 0, sizeof(unsigned long long) + 2 * sizeof(int32_t), s));
@@ -1117,11 +1143,46 @@ extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_nee
                            "displacement (%d,%d) at t=%d, a=%d exceeds sub-grid half widths (%d,%d)",
                            didj[0], didj[1], t, a, h->hx, h->hy);
         }
-    FM_CK(cudaFreeAsync(Kg, s));
     if (h_needed) *h_needed = nnz;
     if (nnz > M->capacity)
         return fm_fail(FM_CAPACITY, "fm_build: entry capacity %llu < %llu needed",
                        (unsigned long long)M->capacity, nnz);
+    return FM_OK;
+}
+
+extern "C" int32_t fm_build(const fm_build_args *h, fm_model *M, uint64_t *h_needed, fm_violation *h_viol,
+                            void *stream)
+{
+    int32_t st = fm_build_launch(h, M, stream);
+    if (st != FM_OK) return st;
+    return fm_build_check(h, M, h_needed, h_viol, stream);
+}
+
+// Obstacle-gate radius on the device (model_builder.py:218-223 with the
+// triangle bound of environment.py:404-419), same arithmetic as the host:
+// per_t = max|mean| (+) sum_m max|coef| (x) max|mode|, bound = max_t per_t,
+// r = ceil(((bound + f_max) * dt) / dx) + 1.
+__global__ void k_gate_radius(fm_grid G, const double *meanmax, const double *coefmax, const double *modemax, int nm,
+                              double f_max, int32_t *out2, double *bound2)
+{
+    if (threadIdx.x >= 2) return;
+    const int c = threadIdx.x;
+    double b = 0.0;
+    for (int t = 0; t < G.nt; ++t) {
+        double per = meanmax[t * 2 + c];
+        for (int m = 0; m < nm; ++m) per = DADD(per, DMUL(coefmax[t * nm + m], modemax[(m * G.nt + t) * 2 + c]));
+        b = t == 0 ? per : fmax(b, per);
+    }
+    const double reach = DDIV(DMUL(DADD(b, f_max), G.dt), G.dx);
+    out2[c] = (int32_t)ceil(reach) + 1;
+    if (bound2) bound2[c] = b;
+}
+
+extern "C" int32_t fm_gate_radius(fm_grid G, const double *meanmax, const double *coefmax, const double *modemax,
+                                  int32_t n_modes, double f_max, int32_t *d_out2, double *d_bound2, void *stream)
+{
+    k_gate_radius<<<1, 32, 0, (cudaStream_t)stream>>>(G, meanmax, coefmax, modemax, n_modes, f_max, d_out2, d_bound2);
+    FM_CK_LAUNCH("k_gate_radius");
     return FM_OK;
 }
 
@@ -1194,6 +1255,7 @@ static int32_t scan_u64(uint64_t *data, int64_t n, cudaStream_t s)
 struct ModelK {
     int nx, ny, nt, nc, na, nr, hx, hy, width, nslot;
     long long n_rows, n_g;
+    unsigned long long capacity;
     const uint64_t *row_ptr;
     const uint16_t *row_nnz;
     const double *reward;
@@ -1208,6 +1270,7 @@ static ModelK model_k(const fm_model *M)
     K.nslot = (2 * M->hx + 1) * (2 * M->hy + 1);
     K.n_rows = M->n_rows; K.n_g = (long long)M->nt * K.nc;
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward; K.entries = M->entries;
+    K.capacity = M->capacity;
     return K;
 }
 
@@ -1315,7 +1378,8 @@ __global__ void __launch_bounds__(256) k_solve_layer(const SolveK S)
         if (cell_ok && a < K.na) {
             const size_t row = ((size_t)t * K.nc + c) * K.na + a;
             const uint64_t p = K.row_ptr[row];
-            const int n = K.row_nnz[row];
+            // an over-capacity build (deferred check) is discarded; never read past the buffer
+            const int n = p + K.row_nnz[row] <= K.capacity ? K.row_nnz[row] : 0;
             double acc = 0.0;   // np.bincount starts every row at +0.0
             for (int k = 0; k < n; ++k) {
                 const uint32_t e = __ldg(K.entries + p + k);

@@ -40,6 +40,10 @@ def plan(env, actions, rcfg, target, buffer: int = 1, device_env: DeviceEnv | No
     denv = device_env if device_env is not None else DeviceEnv.from_host(env)
     sub = subgrid if subgrid is not None else subgrid_from_vmax(denv.velocity_max(), actions.f_max,
                                                                denv.grid, buffer)
-    dm = build_device_model(denv, actions, rcfg, target, sub)
+    # the solve is queued behind the build; the build's census/overflow
+    # check runs once both are in flight (one host round trip)
+    dm = build_device_model(denv, actions, rcfg, target, sub, defer_check=True)
     values, policy = solve_backward(dm)
+    if dm.check():   # capacity miss: the model was rebuilt, solve it again
+        values, policy = solve_backward(dm, values, policy)
     return Plan(subgrid=sub, model=dm, values=values, policy=policy)

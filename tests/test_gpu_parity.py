@@ -277,3 +277,34 @@ def test_workload_subgrid_hints(name):
     env = w.environment()
     sub = fm.compute_subgrid(env.field, w.actions(), env.grid)
     assert (sub.half_width_x, sub.half_width_y) == w.subgrid_hint
+
+
+def test_gate_radius_device_matches_reference_arithmetic():
+    """fm_gate_radius (device) == oracle.gate_radius (numpy, the reference's formula)."""
+    for seed in RANDOM_SEEDS[:20]:
+        env, acts, _, _ = make_random_env(seed)
+        de = DeviceEnv.from_host(env)
+        got = tuple(int(x) for x in de.gate_radius_device(acts.f_max).cpu().numpy())
+        assert got == O.gate_radius(env.field, acts.f_max, env.grid)
+        assert de.velocity_bound() == O.velocity_bound(env.field)
+
+
+def test_planner_deferred_check_and_capacity_retry():
+    """plan() queues the solve behind the build; a too-small entry buffer is
+    detected by the deferred check, rebuilt and re-solved."""
+    env, acts, rcfg, target = make_random_env(7011)
+    de = DeviceEnv.from_host(env)
+    sub = fm.compute_subgrid(env.field, acts, env.grid, device_env=de)
+    dm = build_device_model(de, acts, rcfg, target, sub, capacity_hint=8, defer_check=True)
+    v, p = solve_backward(dm)
+    assert dm.check() is True
+    v, p = solve_backward(dm, v, p)
+    hx, hy = sub.half_width_x, sub.half_width_y
+    om = O.build_model(env, acts, rcfg, target, hx, hy)
+    ov, oa, _, res, _ = O.value_iteration(om)
+    if res == 0.0:
+        assert v.cpu().numpy().tobytes() == ov.tobytes()
+    assert model_digest(dm.to_sparse_model()) == model_digest(om)
+    plan = fm.plan(env, acts, rcfg, target)
+    if res == 0.0:
+        assert plan.values.cpu().numpy().tobytes() == ov.tobytes()

@@ -12,7 +12,7 @@ w = workloads.get(name)
 env = w.environment()
 denv = DeviceEnv.from_host(env)
 for _ in range(reps):
-    denv._vmax = None
+    denv.reset_derived()
     sub = subgrid_from_vmax(denv.velocity_max(), w.f_max, env.grid)
     dm = build_device_model(denv, w.actions(), w.reward_config(), w.target, sub)
     solve_backward(dm)

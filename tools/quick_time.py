@@ -15,7 +15,7 @@ denv = DeviceEnv.from_host(env)
 torch.cuda.synchronize()
 def ev(): return torch.cuda.Event(enable_timing=True)
 for it in range(3):
-    denv._vmax = None
+    denv.reset_derived()
     e0, e1, e2, e3 = ev(), ev(), ev(), ev()
     e0.record()
     vm = denv.velocity_max()
