@@ -112,6 +112,20 @@ typedef struct {
     uint32_t *task_counter;   /* device [1] scratch, zeroed by fm_build      */
     const int32_t *d_gate_r;  /* device [rx, ry] from fm_gate_radius, or NULL
                                  to use rx/ry above                          */
+    /* Optional fast-path enablers (both may be left 0 / negative: the build
+     * is then fully checked per transition).  Neither changes any output.
+     *  h_actions: HOST copy of `actions`.  With it the build proves, per
+     *    launch, whether every per-transition reward is a dyadic value whose
+     *    sequential f64 sum over n_real realizations is exact; if so the
+     *    reward sum (model_builder.py:457-458) is formed from the histogram
+     *    counts instead of per transition (bit-identical by exactness).
+     *  vmax_x, vmax_y: the exact maxima of fm_velocity_max (>= 0), or < 0 if
+     *    unknown.  With them (and h_actions) the build proves by monotonicity
+     *    of rounding that no in-domain landing can leave the sub-grid window
+     *    (no overflow check needed) and that cell indices fit in 2^30, so the
+     *    lean path floors with one round-down add instead of F2I. */
+    const fm_action *h_actions;
+    double vmax_x, vmax_y;
 } fm_build_args;
 
 /* Sub-grid overflow report (message of model_builder.py:433-438). */

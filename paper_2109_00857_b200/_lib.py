@@ -90,7 +90,8 @@ class FmBuildArgs(C.Structure):
                 ("hx", C.c_int32), ("hy", C.c_int32), ("rx", C.c_int32), ("ry", C.c_int32),
                 ("mask_sat", C.c_void_p),
                 ("t0", C.c_int32), ("t1", C.c_int32), ("j0", C.c_int32), ("j1", C.c_int32),
-                ("viol_flags", C.c_void_p), ("task_counter", C.c_void_p), ("d_gate_r", C.c_void_p)]
+                ("viol_flags", C.c_void_p), ("task_counter", C.c_void_p), ("d_gate_r", C.c_void_p),
+                ("h_actions", C.c_void_p), ("vmax_x", C.c_double), ("vmax_y", C.c_double)]
 
 
 class FmViolation(C.Structure):

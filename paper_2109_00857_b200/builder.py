@@ -341,13 +341,18 @@ class DeviceModel:
 
 def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridSpec,
                        t_range: tuple | None = None, j_range: tuple | None = None,
-                       capacity_hint: int | None = None, defer_check: bool = False) -> DeviceModel:
+                       capacity_hint: int | None = None, defer_check: bool = False,
+                       lean: bool = True) -> DeviceModel:
     """Run K_build over slabs t_range x row strip j_range; the model stays in HBM.
 
     With defer_check the kernel is only enqueued: consumers (the backward
     solve) can be queued behind it and ``DeviceModel.check()`` performs the
     census / overflow / capacity check later (it rebuilds on a capacity
-    miss and returns True when it did)."""
+    miss and returns True when it did).
+
+    ``lean=False`` withholds the exact velocity maxima and the host action
+    table, so every transition takes the fully checked path (same output;
+    the parity tests use it to cover both paths)."""
     torch = _torch()
     L = _lib.load()
     grid = denv.grid
@@ -377,14 +382,18 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     counter = torch.zeros(1, dtype=torch.int32, device=dev)
     rw = _lib.FmReward(OBJECTIVE_CODE[rcfg.objective], float(rcfg.c_f), float(rcfg.c_r),
                        float(rcfg.r_term), float(rcfg.r_outbound), ti, tj)
+    # the exact velocity maxima (when this env's sub-grid scan has run) let
+    # the kernel prove the lean path's preconditions; they change no output
+    vmx, vmy = denv.velocity_max() if lean else (-1.0, -1.0)
+    recs = np.ascontiguousarray(recs)
     args = _lib.FmBuildArgs(denv.fm_grid(), denv.fm_env(), rw, d_act.data_ptr(), na, hx, hy, 0, 0,
                             denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr(),
-                            d_gate.data_ptr())
+                            d_gate.data_ptr(), recs.ctypes.data if lean else None, vmx, vmy)
     entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
     dm = DeviceModel(grid=grid, n_actions=na, n_real=denv.n_real, subgrid=subgrid,
                      row_ptr=row_ptr, row_nnz=row_nnz, reward=reward, entries=entries,
                      d_nnz=d_nnz, nnz=0, t_range=(t0, t1), j_range=(j0, j1))
-    dm._pending = (args, (d_act, d_gate, viol, counter, denv))
+    dm._pending = (args, (d_act, d_gate, viol, counter, denv, recs))
     m = dm.fm_model()
     _lib.check(L.fm_build_launch(C.byref(args), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
     if not defer_check:

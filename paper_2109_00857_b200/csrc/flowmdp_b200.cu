@@ -13,7 +13,9 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <atomic>
+#include <cfloat>
 #include <climits>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -310,7 +312,12 @@ extern "C" int32_t fm_mask_sat(const uint8_t *mask, int32_t nt, int32_t ny, int3
 // ---------------------------------------------------------------------------
 // K_build
 // ---------------------------------------------------------------------------
-enum : int { F_DT_ONE = 1, F_OX_ZERO = 2, F_DX_MUL = 4, F_DX_ONE = 8, F_NET = 16 };
+// F_PROVEN: the host proved (fm_build_args.vmax_*) that every in-domain
+//   landing lies inside the row's sub-grid window and every cell coordinate
+//   fits in 2^30 -> lean rows need no window test and floor by magic add.
+// F_CNT: the host proved every reward value dyadic with an exact sequential
+//   sum -> lean rows form the reward sum from the histogram counts.
+enum : int { F_DT_ONE = 1, F_OX_ZERO = 2, F_DX_MUL = 4, F_DX_ONE = 8, F_NET = 16, F_PROVEN = 32, F_CNT = 64 };
 enum : int { RF_DEAD = 1, RF_TERMINAL = 2, RF_GATE = 4, RF_LANDWIN = 8, RF_SEGWIN = 16 };
 
 struct BuildK {
@@ -598,6 +605,105 @@ __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, 
     return ok;
 }
 
+// floor(u) for |u| < 2^31: u + 1.5*2^52 lies in [2^52, 2^53) where the ulp
+// is 1, so the round-down add is exactly 1.5*2^52 + floor(u); its low word
+// is floor(u) in two's complement.  One DADD instead of an F2I (XU pipe,
+// a quarter of the FP64 rate).
+__device__ __forceinline__ int floor_magic(double u)
+{
+    return __double2loint(__dadd_rd(u, 6755399441055744.0));
+}
+
+// One lean transition: landing slot q (OUT for a landing outside the domain
+// in EDGE warps) and, unless F_CNT, its reward.
+template <int FLAGS, bool EDGE>
+__device__ __forceinline__ int lean_transition(const BuildK &K, const RowC &R, const double2 v,
+                                               const double *__restrict__ g_n, int outq, double &rw)
+{
+    double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
+    if (!(FLAGS & F_DT_ONE)) {
+        px = DMUL(px, K.dt);
+        py = DMUL(py, K.dt);
+    }
+    const int i1 = floor_magic(to_cell<FLAGS>(DADD(R.x0, px), K.ox, K.dx, K.inv_dx));
+    const int j1 = floor_magic(to_cell<FLAGS>(DADD(R.y0, py), K.oy, K.dx, K.inv_dx));
+    int q = j1 * K.width + i1;
+    bool out = false;
+    if (EDGE) {
+        out = (unsigned)i1 >= (unsigned)K.nx || (unsigned)j1 >= (unsigned)K.ny;
+        if (out) q = outq;
+    }
+    if (!(FLAGS & F_CNT)) {
+        const bool hit = q == R.tslot;
+        if (FLAGS & F_NET) {
+            const double gd = __ldg(g_n + (out ? 0 : j1 * K.nx + i1));
+            double b = DADD(R.AB, DMUL(K.h_cr, gd));
+            if (!(FLAGS & F_DT_ONE)) b = DMUL(b, K.dt);
+            rw = hit ? DADD(b, K.r_term) : b;
+        } else {
+            rw = hit ? R.base_hit : R.base;
+        }
+        if (EDGE && out) rw = K.r_out;
+    }
+    return q;
+}
+
+// Histogram increment of this lane's u16 counter [q][lane].  FM_HIST_ATOMS:
+// a 32-bit shared-memory reduction on the word holding the counter
+// (hs_word = shared address of that word for q = 0; no read-modify-write
+// dependency chain; counts <= n_real <= 65535 never carry into the
+// neighbouring lane's half).
+__device__ __forceinline__ void hist_inc(uint16_t *h16q, unsigned hs_word, int q, unsigned half_one)
+{
+#ifdef FM_HIST_ATOMS
+    (void)h16q;
+    asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(hs_word + (unsigned)q * 64u), "r"(half_one) : "memory");
+#else
+    (void)hs_word;
+    (void)half_one;
+    h16q[q * 32] += (uint16_t)1;
+#endif
+}
+
+// The realization loop of one chunk for lean rows under F_PROVEN: no
+// obstacle near the warp's rows, every landing inside the window or (EDGE
+// warps) outside the domain -> SINK.  No vote, no rare path.  Reward sum in
+// ascending realization order unless F_CNT (then formed from the counts).
+// Velocities of 4 realizations are loaded before any histogram store so the
+// shared loads are not ordered behind possibly-aliasing stores.
+template <int FLAGS, bool EDGE>
+__device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, const double2 *vrow, int nk,
+                                                const double *__restrict__ g_n, uint16_t *h16q, int outq, double &S,
+                                                unsigned half_one)
+{
+    const unsigned hs_word = (unsigned)__cvta_generic_to_shared(h16q) & ~3u;
+    int k = 0;
+    for (; k + 4 <= nk; k += 4) {
+        const double2 v0 = vrow[k], v1 = vrow[k + 1], v2 = vrow[k + 2], v3 = vrow[k + 3];
+        double w0, w1, w2, w3;
+        const int q0 = lean_transition<FLAGS, EDGE>(K, R, v0, g_n, outq, w0);
+        const int q1 = lean_transition<FLAGS, EDGE>(K, R, v1, g_n, outq, w1);
+        const int q2 = lean_transition<FLAGS, EDGE>(K, R, v2, g_n, outq, w2);
+        const int q3 = lean_transition<FLAGS, EDGE>(K, R, v3, g_n, outq, w3);
+        if (!(FLAGS & F_CNT)) {   // ascending realization order (model_builder.py:457-458)
+            S = DADD(S, w0);
+            S = DADD(S, w1);
+            S = DADD(S, w2);
+            S = DADD(S, w3);
+        }
+        hist_inc(h16q, hs_word, q0, half_one);
+        hist_inc(h16q, hs_word, q1, half_one);
+        hist_inc(h16q, hs_word, q2, half_one);
+        hist_inc(h16q, hs_word, q3, half_one);
+    }
+    for (; k < nk; ++k) {
+        double w0;
+        const int q0 = lean_transition<FLAGS, EDGE>(K, R, vrow[k], g_n, outq, w0);
+        if (!(FLAGS & F_CNT)) S = DADD(S, w0);
+        hist_inc(h16q, hs_word, q0, half_one);
+    }
+}
+
 // The realization loop of one chunk for the row lanes: 4 independent
 // transitions per iteration in straight-line code (interleaved by the
 // compiler), one warp vote to divert rare lanes, reward sums in ascending r.
@@ -687,6 +793,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
     const int cs_rec = lane / RW, rr = lane - cs_rec * RW;
     const bool rec_lane = lane < CW * RW;
     const int nslot = K.nslot, W = K.width;
+    const unsigned half_one = 1u << ((lane & 1) * 16);   // this lane's u16 half of a counter word
     // this lane's first (realization, mode) element of a coefficient chunk and
     // the per-step increments (element index advances by 32 each step)
     const int e_r0 = nm ? lane / nm : 0, e_m0 = nm ? lane - (lane / nm) * nm : 0;
@@ -890,6 +997,11 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
                         else
                             chunk_rows<FLAGS, false, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
                                                            viol);
+                    } else if (FLAGS & F_PROVEN) {
+                        if (edge)
+                            chunk_rows_lean<FLAGS, true>(K, Rf, vrow, nk, g_n, h16q, outq, S, half_one);
+                        else
+                            chunk_rows_lean<FLAGS, false>(K, Rf, vrow, nk, g_n, h16q, outq, S, half_one);
                     } else {
                         if (edge)
                             chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
@@ -900,6 +1012,17 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
                     }
                 }
                 __syncwarp();
+            }
+            if ((FLAGS & F_CNT) && !obst && row_ok) {
+                // exact reward sum from the counts (F_CNT): every partial sum
+                // of the reference's sequential loop is exactly representable,
+                // so it equals n_norm*base + n_hit*base_hit + n_out*r_out;
+                // + 0.0 turns a -0.0 into the loop's +0.0
+                const int n_out = h16[nslot * 32], n_hit = R.tslot >= 0 ? h16[R.tslot * 32] : 0;
+                const int n_norm = nr - n_out - n_hit;
+                S = DADD(DADD(DADD(DMUL((double)n_norm, R.base), DMUL((double)n_hit, R.base_hit)),
+                              DMUL((double)n_out, K.r_out)),
+                         0.0);
             }
         }
 
@@ -994,6 +1117,20 @@ static int32_t launch_build_t(const BuildK &K, const BuildK *Kg, size_t smem, cu
 
 static int32_t launch_build(const BuildK &K, const BuildK *Kg, int flags, size_t smem, cudaStream_t s)
 {
+    if (flags & F_PROVEN) {
+        // lean variants exist for the identity geometry (dt = dx = 1, origin
+        // 0) and the general one; dropping identity flags never changes a
+        // result (x*1, x/1, x-0 are exact)
+        const int geo = (flags & 15) == (F_DT_ONE | F_OX_ZERO | F_DX_ONE) ? (flags & 15) : 0;
+        switch (geo | (flags & (F_NET | F_PROVEN | F_CNT))) {
+#define FM_CASE(F) \
+    case F: return launch_build_t<F>(K, Kg, smem, s);
+            FM_CASE(11 | F_PROVEN) FM_CASE(11 | F_PROVEN | F_CNT) FM_CASE(11 | F_PROVEN | F_NET)
+            FM_CASE(F_PROVEN) FM_CASE(F_PROVEN | F_CNT) FM_CASE(F_PROVEN | F_NET)
+#undef FM_CASE
+        }
+        return fm_fail(FM_BAD_ARG, "k_build: bad flags %d", flags);
+    }
     switch (flags) {
 #define FM_CASE(F) \
     case F: return launch_build_t<F>(K, Kg, smem, s);
@@ -1014,6 +1151,75 @@ static bool is_pow2(double x)
 }
 
 static int align16(int x) { return (x + 15) & ~15; }
+
+// One axis of the lean-path proof.  reach = fl(fl(vmax + amax) * dt) bounds
+// |fl(fl(v + a) * dt)| for every transition (|v| <= vmax exactly: it is the
+// maximum of these very reconstructions; rounding is monotone), so
+// x1 = fl(x0 + p) lies in [fl(x0 - reach), fl(x0 + reach)] and, by
+// monotonicity of (x - o) / dx and floor, the landing index lies between the
+// floors of the two ends.  Checked for every source index of the axis.
+static bool prove_axis(int n, double o, double dx, double reach, int hw)
+{
+    for (int c = 0; c < n; ++c) {
+        const double x0 = o + ((double)c + 0.5) * dx;   // environment.py:99-100
+        const double ulo = ((x0 - reach) - o) / dx, uhi = ((x0 + reach) - o) / dx;
+        if (!(fabs(ulo) < 0x1p30 && fabs(uhi) < 0x1p30)) return false;
+        if (floor(ulo) - c < -hw || floor(uhi) - c > hw) return false;
+    }
+    return true;
+}
+
+static bool prove_lean(const fm_build_args *h)
+{
+    const double vx = h->vmax_x, vy = h->vmax_y;
+    if (!(vx >= 0.0 && vy >= 0.0 && std::isfinite(vx) && std::isfinite(vy))) return false;
+    double ax = 0.0, ay = 0.0;
+    for (int a = 0; a < h->n_actions; ++a) {
+        const double x = fabs(h->h_actions[a].ax), y = fabs(h->h_actions[a].ay);
+        if (!(x <= DBL_MAX && y <= DBL_MAX)) return false;
+        ax = x > ax ? x : ax;
+        ay = y > ay ? y : ay;
+    }
+    const fm_grid &G = h->grid;
+    const double rx = (vx + ax) * G.dt, ry = (vy + ay) * G.dt;
+    return std::isfinite(rx) && std::isfinite(ry) && prove_axis(G.nx, G.ox, G.dx, rx, h->hx) &&
+           prove_axis(G.ny, G.oy, G.dx, ry, h->hy);
+}
+
+// Smallest k >= 0 with v * 2^k an integer (v finite), or -1.
+static int dyadic_scale(double v)
+{
+    if (v == 0.0) return 0;
+    if (!std::isfinite(v)) return -1;
+    int e;
+    const double f = frexp(fabs(v), &e);               // v = f 2^e, f in [0.5, 1)
+    uint64_t m = (uint64_t)ldexp(f, 53);               // exact 53-bit mantissa
+    const int tz = __builtin_ctzll(m);
+    const int k = 53 - e - tz;
+    return k > 0 ? k : 0;
+}
+
+// F_CNT precondition: every per-transition reward value (base, base_hit per
+// action, r_outbound, 0) is an integer multiple of 2^-K and
+// n_real * max|value| * 2^K <= 2^52, so every partial sum of the
+// reference's sequential loop, and each count * value, is exact.
+static bool rewards_sum_exactly(const fm_build_args *h)
+{
+    std::vector<double> vals{h->reward.r_outbound, 0.0};
+    for (int a = 0; a < h->n_actions; ++a) {
+        vals.push_back(h->h_actions[a].base);
+        vals.push_back(h->h_actions[a].base_hit);
+    }
+    int K = 0;
+    double mx = 0.0;
+    for (double v : vals) {
+        const int k = dyadic_scale(v);
+        if (k < 0 || k > 900) return false;
+        K = k > K ? k : K;
+        mx = fabs(v) > mx ? fabs(v) : mx;
+    }
+    return ldexp(mx, K) * (double)h->env.n_real <= 0x1p52;
+}
 
 // validates the arguments and fills the kernel parameter block + flags
 static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K, int &flags)
@@ -1079,6 +1285,10 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     if (K.obj == FM_OBJ_NET_ENERGY) flags |= F_NET;
 
     K.gate_r = h->d_gate_r;
+    if (h->h_actions && prove_lean(h)) {
+        flags |= F_PROVEN;
+        if (K.obj != FM_OBJ_NET_ENERGY && rewards_sum_exactly(h)) flags |= F_CNT;
+    }
     return FM_OK;
 }
 

@@ -59,6 +59,9 @@ def _gpu_case(env, acts, rcfg, target, rec=None):
     denv = ctx.device_env()
     dm = build_device_model(denv, acts, rcfg, target, sub)
     vals, pol = solve_backward(dm)
+    # the fully checked per-transition path gives the same model
+    dmc = build_device_model(denv, acts, rcfg, target, sub, lean=False)
+    assert model_digest(dmc.to_sparse_model()) == model_digest(om)
     if ores == 0.0:
         assert sha(vals.cpu().numpy()) == sha(ov)
         assert sha(pol.cpu().numpy().view(np.uint16)) == sha(oa)
@@ -172,11 +175,13 @@ def test_strip_and_slab_sharding_union_equals_full():
     assert torch.equal(nnz, full.row_nnz) and torch.equal(rew, full.reward)
 
 
-def test_paper_scale_slabs_vs_oracle():
-    """C2 geometry (100x100, 16 actions) with 1000 realizations: every slab
-    on the GPU, three slabs (first, middle, horizon) on the oracle."""
+@pytest.mark.parametrize("name", ["paper", "paper_energy", "paper_net_energy"])
+def test_paper_scale_slabs_vs_oracle(name):
+    """C2/C3/C4 geometry (100x100, 16 actions; time / energy / net_energy with
+    two moving obstacles) with 1000 realizations: every slab on the GPU,
+    three slabs (first, middle, horizon) on the oracle."""
     from paper_2109_00857_b200 import workloads
-    w = workloads.get("paper").with_(grid=workloads.GridSpec(nx=100, ny=100, nt=100, dx=1.0, dt=1.0),
+    w = workloads.get(name).with_(grid=workloads.GridSpec(nx=100, ny=100, nt=100, dx=1.0, dt=1.0),
                                      n_realizations=1000)
     env = w.environment()
     acts, rcfg, target = w.actions(), w.reward_config(), w.target
