@@ -614,6 +614,36 @@ __device__ __forceinline__ int floor_magic(double u)
     return __double2loint(__dadd_rd(u, 6755399441055744.0));
 }
 
+// Reconstruction of this recon lane's realizations of one chunk for 8 modes
+// (environment.py:293-297: v = mean; v += c_m * mode_m for ascending m, two
+// roundings per term): the cell's modes stay in registers, two
+// realizations per pass share them, coefficients come as [pair][r] double2.
+__device__ __forceinline__ void recon_m8(const double2 *md, const double2 *c2, double2 mu, int RC, int RW, int RPL,
+                                         int rr, int n_left, double2 *vout)
+{
+    double2 m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = md[i];
+    for (int p = 0; p < RPL; p += 2) {
+        const int rl0 = p * RW + rr, rl1 = p + 1 < RPL ? rl0 + RW : rl0;   // odd RPL: recompute rl0
+        double x0 = mu.x, y0 = mu.y, x1 = mu.x, y1 = mu.y;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 k0 = c2[q * RC + rl0], k1 = c2[q * RC + rl1];
+            x0 = DADD(x0, DMUL(k0.x, m[2 * q].x));
+            y0 = DADD(y0, DMUL(k0.x, m[2 * q].y));
+            x1 = DADD(x1, DMUL(k1.x, m[2 * q].x));
+            y1 = DADD(y1, DMUL(k1.x, m[2 * q].y));
+            x0 = DADD(x0, DMUL(k0.y, m[2 * q + 1].x));
+            y0 = DADD(y0, DMUL(k0.y, m[2 * q + 1].y));
+            x1 = DADD(x1, DMUL(k1.y, m[2 * q + 1].x));
+            y1 = DADD(y1, DMUL(k1.y, m[2 * q + 1].y));
+        }
+        if (rl0 < n_left) vout[rl0] = make_double2(x0, y0);
+        if (rl1 != rl0 && rl1 < n_left) vout[rl1] = make_double2(x1, y1);
+    }
+}
+
 // One lean transition: landing slot q (OUT for a landing outside the domain
 // in EDGE warps) and, unless F_CNT, its reward.
 template <int FLAGS, bool EDGE>
@@ -669,7 +699,7 @@ __device__ __forceinline__ void hist_inc(uint16_t *h16q, unsigned hs_word, int q
 // obstacle near the warp's rows, every landing inside the window or (EDGE
 // warps) outside the domain -> SINK.  No vote, no rare path.  Reward sum in
 // ascending realization order unless F_CNT (then formed from the counts).
-// Velocities of 4 realizations are loaded before any histogram store so the
+// Velocities of U realizations are loaded before any histogram store so the
 // shared loads are not ordered behind possibly-aliasing stores.
 template <int FLAGS, bool EDGE>
 __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, const double2 *vrow, int nk,
@@ -677,24 +707,25 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
                                                 unsigned half_one)
 {
     const unsigned hs_word = (unsigned)__cvta_generic_to_shared(h16q) & ~3u;
+#ifndef FM_LEAN_U
+#define FM_LEAN_U 8
+#endif
+    constexpr int U = FM_LEAN_U;
     int k = 0;
-    for (; k + 4 <= nk; k += 4) {
-        const double2 v0 = vrow[k], v1 = vrow[k + 1], v2 = vrow[k + 2], v3 = vrow[k + 3];
-        double w0, w1, w2, w3;
-        const int q0 = lean_transition<FLAGS, EDGE>(K, R, v0, g_n, outq, w0);
-        const int q1 = lean_transition<FLAGS, EDGE>(K, R, v1, g_n, outq, w1);
-        const int q2 = lean_transition<FLAGS, EDGE>(K, R, v2, g_n, outq, w2);
-        const int q3 = lean_transition<FLAGS, EDGE>(K, R, v3, g_n, outq, w3);
+    for (; k + U <= nk; k += U) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = vrow[k + u];
+        int q[U];
+        double w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) q[u] = lean_transition<FLAGS, EDGE>(K, R, v[u], g_n, outq, w[u]);
         if (!(FLAGS & F_CNT)) {   // ascending realization order (model_builder.py:457-458)
-            S = DADD(S, w0);
-            S = DADD(S, w1);
-            S = DADD(S, w2);
-            S = DADD(S, w3);
+#pragma unroll
+            for (int u = 0; u < U; ++u) S = DADD(S, w[u]);
         }
-        hist_inc(h16q, hs_word, q0, half_one);
-        hist_inc(h16q, hs_word, q1, half_one);
-        hist_inc(h16q, hs_word, q2, half_one);
-        hist_inc(h16q, hs_word, q3, half_one);
+#pragma unroll
+        for (int u = 0; u < U; ++u) hist_inc(h16q, hs_word, q[u], half_one);
     }
     for (; k < nk; ++k) {
         double w0;
@@ -798,6 +829,10 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
     // the per-step increments (element index advances by 32 each step)
     const int e_r0 = nm ? lane / nm : 0, e_m0 = nm ? lane - (lane / nm) * nm : 0;
     const int e_dr = nm ? 32 / nm : 0, e_dm = nm ? 32 - (32 / nm) * nm : 0;
+    // same for the paired (16-byte) layout: element = (realization, mode pair)
+    const int np2 = nm >> 1;
+    const int p_r0 = np2 ? lane / np2 : 0, p_p0 = np2 ? lane - (lane / np2) * np2 : 0;
+    const int p_dr = np2 ? 32 / np2 : 0, p_dp = np2 ? 32 - (32 / np2) * np2 : 0;
 
     for (;;) {
         unsigned task = 0;
@@ -933,10 +968,17 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
                 const double *src = cf_t + (size_t)r0 * nm;
                 if (pairs) {
                     // 16-byte copies: (realization rl, modes 2p..2p+1) -> coef2[p][rl]
-                    const int np = nm >> 1, n_el = nrc * np;
+                    // incremental (realization, pair) walk: no integer division
+                    const int n_el = nrc * np2;
+                    int rl = p_r0, pp = p_p0;
                     for (int i = lane; i < n_el; i += 32) {
-                        const int rl = i / np, pp = i - rl * np;
-                        cp_async16(coefT + ((size_t)pp * RC + rl) * 2, src + (size_t)rl * nm + 2 * pp);
+                        cp_async16(coefT + (pp * RC + rl) * 2, src + rl * nm + 2 * pp);
+                        rl += p_dr;
+                        pp += p_dp;
+                        if (pp >= np2) {
+                            pp -= np2;
+                            ++rl;
+                        }
                     }
                 } else {
                     const int n_el = nrc * nm;
@@ -958,7 +1000,10 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
             for (int r0 = 0; r0 < nr; r0 += RC) {
                 cp_async_wait_all();
                 __syncwarp();
-                if (rec_ok) {
+                if (rec_ok && pairs && nm == 8) {
+                    recon_m8(modes_s + cs_rec * 8, reinterpret_cast<const double2 *>(coefT), mu, RC, RW, RPL, rr,
+                             nr - r0, vbuf + cs_rec * (RC + 1));
+                } else if (rec_ok) {
                     const double2 *md = modes_s + cs_rec * nm;
                     for (int p = 0; p < RPL; ++p) {
                         const int rl = p * RW + rr;

@@ -14,7 +14,8 @@ acts, rcfg = w.actions(), w.reward_config()
 denv = DeviceEnv.from_host(env)
 torch.cuda.synchronize()
 def ev(): return torch.cuda.Event(enable_timing=True)
-for it in range(3):
+res = []
+for it in range(int(os.environ.get('QT_ITERS', 6))):
     denv.reset_derived()
     e0, e1, e2, e3 = ev(), ev(), ev(), ev()
     e0.record()
@@ -26,5 +27,8 @@ for it in range(3):
     v, p = solve_backward(dm)
     e3.record()
     torch.cuda.synchronize()
-    print(f"{name} it{it} sub={sub} nnz={dm.nnz} vmax_ms={e0.elapsed_time(e1):.2f} build_ms={e1.elapsed_time(e2):.2f} "
-          f"solve_ms={e2.elapsed_time(e3):.2f} U={w.transitions:.3e} trans/s={w.transitions/(e1.elapsed_time(e2)/1e3):.3e}", flush=True)
+    res.append((e1.elapsed_time(e2), e0.elapsed_time(e1), e2.elapsed_time(e3)))
+b = sorted(r[0] for r in res[1:])
+print(f"{name} sub={sub} nnz={dm.nnz} build_ms min={b[0]:.2f} med={b[len(b)//2]:.2f} "
+      f"vmax_ms={min(r[1] for r in res):.2f} solve_ms={min(r[2] for r in res):.2f} "
+      f"trans/s={w.transitions/(b[0]/1e3):.3e}", flush=True)
