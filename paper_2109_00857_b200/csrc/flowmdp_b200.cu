@@ -87,6 +87,27 @@ static int sm_count()
     return n;
 }
 
+// Development counters (-DFM_STATS): [0] rare transitions, [1] exact
+// segment samplings, [2] segment samples, [3] transitions in obstacle warps,
+// [4] transitions in lean warps.  Not part of the ABI header.
+#ifdef FM_STATS
+__device__ unsigned long long g_fm_stats[8];
+#define FM_STAT(i, n) atomicAdd(&g_fm_stats[i], (unsigned long long)(n))
+#else
+#define FM_STAT(i, n) ((void)0)
+#endif
+extern "C" int32_t fm_dev_stats(uint64_t *h_out8)
+{
+#ifdef FM_STATS
+    FM_CK(cudaMemcpyFromSymbol(h_out8, g_fm_stats, 64));
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    FM_CK(cudaMemcpyToSymbol(g_fm_stats, z, 64));
+#else
+    for (int i = 0; i < 8; ++i) h_out8[i] = 0;
+#endif
+    return FM_OK;
+}
+
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------
@@ -396,6 +417,8 @@ __device__ __forceinline__ bool seg_blocked(const BuildK &K, int t, double p0x, 
     double ns = ceil(DDIV(len, K.half_dx));
     if (!(ns >= 1.0)) ns = 1.0;
     const long long n = (long long)ns;
+    FM_STAT(1, 1);
+    FM_STAT(2, n + 1);
     const uint8_t *mt = K.mask + (size_t)t * K.nc;
     for (long long q = 0; q <= n; ++q) {
         double frac = DDIV((double)q, ns);
@@ -543,6 +566,7 @@ template <int FLAGS>
 __device__ __noinline__ SlowOut rare_transition(const BuildK *__restrict__ Kg, int t, const RowC R, const double2 v)
 {
     const BuildK &K = *Kg;
+    FM_STAT(0, 1);
     const double *g_n = K.g + (size_t)(t + 1) * K.nc;
     const uint8_t *mask_n = K.mask + (size_t)(t + 1) * K.nc;
     SlowOut o;
@@ -552,6 +576,15 @@ __device__ __noinline__ SlowOut rare_transition(const BuildK *__restrict__ Kg, i
     step_one<FLAGS, true>(K, Kg, t, Ra, v, g_n, mask_n, o.slot, o.rw, o.viol);
     o.slot -= R.soff;
     return o;
+}
+
+// floor(u) for |u| < 2^31: u + 1.5*2^52 lies in [2^52, 2^53) where the ulp
+// is 1, so the round-down add is exactly 1.5*2^52 + floor(u); its low word
+// is floor(u) in two's complement.  One DADD instead of an F2I (XU pipe,
+// a quarter of the FP64 rate).
+__device__ __forceinline__ int floor_magic(double u)
+{
+    return __double2loint(__dadd_rd(u, 6755399441055744.0));
 }
 
 // Branch-free fast transition.  Valid when the landing is inside the row's
@@ -570,9 +603,18 @@ __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, 
         py = DMUL(py, K.dt);
     }
     const double x1 = DADD(R.x0, px), y1 = DADD(R.y0, py);
-    const int i1 = __double2int_rd(to_cell<FLAGS>(x1, K.ox, K.dx, K.inv_dx));
-    const int j1 = __double2int_rd(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx));
-    const bool inwin = (unsigned)(i1 - R.ilc) <= (unsigned)R.wi && (unsigned)(j1 - R.jlc) <= (unsigned)R.wj;
+    int i1, j1;
+    bool inwin;
+    if (FLAGS & F_PROVEN) {
+        // proven: an in-domain landing is inside the (clipped) window
+        i1 = floor_magic(to_cell<FLAGS>(x1, K.ox, K.dx, K.inv_dx));
+        j1 = floor_magic(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx));
+        inwin = !EDGE || ((unsigned)i1 < (unsigned)K.nx && (unsigned)j1 < (unsigned)K.ny);
+    } else {
+        i1 = __double2int_rd(to_cell<FLAGS>(x1, K.ox, K.dx, K.inv_dx));
+        j1 = __double2int_rd(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx));
+        inwin = (unsigned)(i1 - R.ilc) <= (unsigned)R.wi && (unsigned)(j1 - R.jlc) <= (unsigned)R.wj;
+    }
     q = j1 * K.width + i1;                       // slot - soff
     const bool hit = q == R.tslot;               // R.tslot holds tslot - soff
     if (FLAGS & F_NET) {
@@ -603,15 +645,6 @@ __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, 
         ok = ok || out;
     }
     return ok;
-}
-
-// floor(u) for |u| < 2^31: u + 1.5*2^52 lies in [2^52, 2^53) where the ulp
-// is 1, so the round-down add is exactly 1.5*2^52 + floor(u); its low word
-// is floor(u) in two's complement.  One DADD instead of an F2I (XU pipe,
-// a quarter of the FP64 rate).
-__device__ __forceinline__ int floor_magic(double u)
-{
-    return __double2loint(__dadd_rd(u, 6755399441055744.0));
 }
 
 // Reconstruction of this recon lane's realizations of one chunk for 8 modes
@@ -678,6 +711,13 @@ __device__ __forceinline__ int lean_transition(const BuildK &K, const RowC &R, c
     return q;
 }
 
+// Shared-memory reductions for the lean histogram updates are the default
+// (A/B at C2: 103 ms vs 111 ms for load/add/store, whose dependency chain
+// serialises the 8 updates of a batch); -DFM_HIST_RMW selects the latter.
+#if !defined(FM_HIST_RMW) && !defined(FM_HIST_ATOMS)
+#define FM_HIST_ATOMS
+#endif
+
 // Histogram increment of this lane's u16 counter [q][lane].  FM_HIST_ATOMS:
 // a 32-bit shared-memory reduction on the word holding the counter
 // (hs_word = shared address of that word for q = 0; no read-modify-write
@@ -724,8 +764,21 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
 #pragma unroll
             for (int u = 0; u < U; ++u) S = DADD(S, w[u]);
         }
+#if defined(FM_HIST_PAIR) && !defined(FM_HIST_ATOMS)
+        // two counters per step: both loads issue before either store, so the
+        // read-modify-write chain is half as long; equal slots add 2 (the
+        // second store, which lands last, carries the sum)
+#pragma unroll
+        for (int u = 0; u < U; u += 2) {
+            uint16_t *pa = h16q + q[u] * 32, *pb = h16q + q[u + 1] * 32;
+            const unsigned ca = *pa, cb = *pb;
+            *pa = (uint16_t)(ca + 1u);
+            *pb = (uint16_t)(cb + 1u + (q[u] == q[u + 1] ? 1u : 0u));
+        }
+#else
 #pragma unroll
         for (int u = 0; u < U; ++u) hist_inc(h16q, hs_word, q[u], half_one);
+#endif
     }
     for (; k < nk; ++k) {
         double w0;
@@ -970,6 +1023,15 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
                     // 16-byte copies: (realization rl, modes 2p..2p+1) -> coef2[p][rl]
                     // incremental (realization, pair) walk: no integer division
                     const int n_el = nrc * np2;
+                    if (p_dp == 0) {
+                        // np2 divides 32: this lane's pair is fixed and its
+                        // realization advances by p_dr per step
+                        const double *sp = src + p_r0 * nm + 2 * p_p0;
+                        double *dp = coefT + (p_p0 * RC + p_r0) * 2;
+                        for (int i = lane; i < n_el; i += 32, sp += p_dr * nm, dp += 2 * p_dr) cp_async16(dp, sp);
+                        cp_async_commit();
+                        return;
+                    }
                     int rl = p_r0, pp = p_p0;
                     for (int i = lane; i < n_el; i += 32) {
                         cp_async16(coefT + (pp * RC + rl) * 2, src + rl * nm + 2 * pp);
@@ -1035,6 +1097,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
                 if (r0 + RC < nr) issue_chunk(r0 + RC);   // lands while the rows work
                 const int nk = min(RC, nr - r0);
                 if (row_ok) {
+                    FM_STAT(obst ? 3 : 4, nk);
                     if (obst) {
                         if (edge)
                             chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
