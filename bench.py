@@ -220,6 +220,7 @@ def run_ours(args):
     policy = torch.zeros(n_g, dtype=torch.int16, device="cuda")
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     build_ev = []
+    prev = {}
 
     def step(de):
         de.reset_derived()                       # sub-grid and gate statistics are recomputed every step
@@ -227,7 +228,9 @@ def run_ours(args):
         sub = subgrid_from_vmax(vm, acts.f_max, g, w.buffer)
         b0, b1 = ev(), ev()
         b0.record()
-        dm = build_device_model(de, acts, rcfg, w.target, sub, j_range=(j0, j1), defer_check=True)
+        dm = build_device_model(de, acts, rcfg, w.target, sub, j_range=(j0, j1), defer_check=True,
+                                reuse=prev.pop("dm", None))   # the previous step's buffers: no allocation
+        prev["dm"] = dm
         b1.record()
         if world > 1:
             values.zero_()

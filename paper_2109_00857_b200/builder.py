@@ -51,6 +51,15 @@ class DeviceEnv:
     n_real: int
     _vbound: dict = field(default_factory=dict)
     _vmax: tuple | None = None
+    _acts: dict = field(default_factory=dict)
+
+    def action_table(self, recs: np.ndarray):
+        """Device copy of an action-record table (cached by content)."""
+        key = recs.tobytes()
+        if key not in self._acts:
+            torch = _torch()
+            self._acts[key] = torch.from_numpy(np.array(recs)).to(self.mean.device)
+        return self._acts[key]
 
     @classmethod
     def from_host(cls, env, device=None, non_blocking: bool = False):
@@ -262,6 +271,7 @@ class DeviceModel:
         return self.grid.nt * self.grid.nx * self.grid.ny + 1
 
     _pending: tuple | None = None
+    _scratch: tuple | None = None
 
     def check(self) -> bool:
         """Finish a (deferred) build: census, sub-grid overflow (raises the
@@ -342,7 +352,7 @@ class DeviceModel:
 def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridSpec,
                        t_range: tuple | None = None, j_range: tuple | None = None,
                        capacity_hint: int | None = None, defer_check: bool = False,
-                       lean: bool = True) -> DeviceModel:
+                       lean: bool = True, reuse: DeviceModel | None = None) -> DeviceModel:
     """Run K_build over slabs t_range x row strip j_range; the model stays in HBM.
 
     With defer_check the kernel is only enqueued: consumers (the backward
@@ -352,7 +362,11 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
 
     ``lean=False`` withholds the exact velocity maxima and the host action
     table, so every transition takes the fully checked path (same output;
-    the parity tests use it to cover both paths)."""
+    the parity tests use it to cover both paths).
+
+    ``reuse`` hands over the buffers of a previous model of the same problem
+    shape (that model must not be used afterwards): repeated planner steps
+    then allocate nothing."""
     torch = _torch()
     L = _lib.load()
     grid = denv.grid
@@ -365,7 +379,7 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     dev = denv.mean.device
     recs = action_records(actions, rcfg, grid)
     na = recs.shape[0]
-    d_act = torch.from_numpy(recs).pin_memory().to(dev, non_blocking=True)
+    d_act = denv.action_table(recs)
     d_gate = denv.gate_radius_device(float(actions.f_max))
     hx, hy = subgrid.half_width_x, subgrid.half_width_y
     nc = grid.nx * grid.ny
@@ -373,13 +387,25 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     active_rows = (t1 - t0) * (j1 - j0) * grid.nx * na
     n_slot1 = (2 * hx + 1) * (2 * hy + 1) + 1
     cap = capacity_hint if capacity_hint else active_rows * min(n_slot1, denv.n_real, 6) + 1024
-    alloc = torch.empty if full else torch.zeros
-    row_ptr = torch.empty(n_rows, dtype=torch.int64, device=dev)
-    row_nnz = alloc(n_rows, dtype=torch.int16, device=dev)
-    reward = alloc(n_rows, dtype=torch.float64, device=dev)
-    d_nnz = torch.zeros(1, dtype=torch.int64, device=dev)
-    viol = torch.zeros(grid.nt * na, dtype=torch.int32, device=dev)
-    counter = torch.zeros(1, dtype=torch.int32, device=dev)
+    if reuse is not None and reuse.row_ptr.numel() == n_rows and reuse.row_ptr.device == dev:
+        row_ptr, row_nnz, reward, d_nnz = reuse.row_ptr, reuse.row_nnz, reuse.reward, reuse.d_nnz
+        d_nnz.zero_()
+        if not full:
+            row_nnz.zero_()
+            reward.zero_()
+        entries = reuse.entries if reuse.entries.numel() >= cap else None
+        viol, counter = reuse._scratch
+        viol.zero_()
+        reuse._pending = None
+    else:
+        alloc = torch.empty if full else torch.zeros
+        row_ptr = torch.empty(n_rows, dtype=torch.int64, device=dev)
+        row_nnz = alloc(n_rows, dtype=torch.int16, device=dev)
+        reward = alloc(n_rows, dtype=torch.float64, device=dev)
+        d_nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+        viol = torch.zeros(grid.nt * na, dtype=torch.int32, device=dev)
+        counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        entries = None
     rw = _lib.FmReward(OBJECTIVE_CODE[rcfg.objective], float(rcfg.c_f), float(rcfg.c_r),
                        float(rcfg.r_term), float(rcfg.r_outbound), ti, tj)
     # the exact velocity maxima (when this env's sub-grid scan has run) let
@@ -389,11 +415,13 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     args = _lib.FmBuildArgs(denv.fm_grid(), denv.fm_env(), rw, d_act.data_ptr(), na, hx, hy, 0, 0,
                             denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr(),
                             d_gate.data_ptr(), recs.ctypes.data if lean else None, vmx, vmy)
-    entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
+    if entries is None:
+        entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
     dm = DeviceModel(grid=grid, n_actions=na, n_real=denv.n_real, subgrid=subgrid,
                      row_ptr=row_ptr, row_nnz=row_nnz, reward=reward, entries=entries,
                      d_nnz=d_nnz, nnz=0, t_range=(t0, t1), j_range=(j0, j1))
     dm._pending = (args, (d_act, d_gate, viol, counter, denv, recs))
+    dm._scratch = (viol, counter)
     m = dm.fm_model()
     _lib.check(L.fm_build_launch(C.byref(args), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
     if not defer_check:

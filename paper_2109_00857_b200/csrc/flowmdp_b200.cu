@@ -108,6 +108,23 @@ extern "C" int32_t fm_dev_stats(uint64_t *h_out8)
     return FM_OK;
 }
 
+// Keep the stream-ordered pool's memory across synchronisations (the
+// default release threshold of 0 hands it back at every sync, so the next
+// cudaMallocAsync of a planner step would map fresh pages).
+static void pool_keep()
+{
+    static bool done = false;
+    if (done) return;
+    done = true;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------
@@ -149,6 +166,19 @@ __device__ __noinline__ double vmax_exact_component(const fm_grid G, const fm_en
     return fabs(v);
 }
 
+// packed 2 x FP32 fused multiply-add (sm_100 FFMA2): a * (b.x, b.y) + c
+__device__ __forceinline__ float2 ffma2_bcast(float a, float2 b, float2 c)
+{
+    unsigned long long r;
+    const float2 aa = make_float2(a, a);
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const unsigned long long *>(&aa)),
+          "l"(*reinterpret_cast<const unsigned long long *>(&b)),
+          "l"(*reinterpret_cast<const unsigned long long *>(&c)));
+    return *reinterpret_cast<float2 *>(&r);
+}
+
 template <int NMX>
 __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_block, const double *cmax, double *out2)
 {
@@ -162,6 +192,7 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_blo
     const bool ok = c < nc;
     float mx32 = 0.f, my32 = 0.f;
     float dx32[NMX], dy32[NMX];
+    float2 d32[NMX];
     double Tx = 0.0, Ty = 0.0;
     if (ok) {
         const double2 mu = *reinterpret_cast<const double2 *>(E.mean + ((size_t)t * nc + c) * 2);
@@ -172,10 +203,12 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_blo
 #pragma unroll
         for (int m = 0; m < NMX; ++m) {
             dx32[m] = dy32[m] = 0.f;
+            d32[m] = make_float2(0.f, 0.f);
             if (m < nm) {
                 const double2 md = *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + c) * 2);
                 dx32[m] = (float)md.x;
                 dy32[m] = (float)md.y;
+                d32[m] = make_float2(dx32[m], dy32[m]);
                 const double cm = cmax[(size_t)t * nm + m];
                 Tx += fabs(md.x) * cm;
                 Ty += fabs(md.y) * cm;
@@ -189,33 +222,57 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_blo
     for (int r0 = r_lo; r0 < r_hi; r0 += kVmaxChunk) {
         const int n = min(kVmaxChunk, r_hi - r0);
         __syncthreads();
-        for (int i = threadIdx.x; i < n * nm; i += blockDim.x) {
-            const int k = i / nm, m = i - (i / nm) * nm;
-            cs[k][m] = (float)E.coeffs[((size_t)t * E.n_real + r0 + k) * nm + m];
+        for (int i = threadIdx.x; i < n * NMX; i += blockDim.x) {
+            const int k = i / NMX, m = i % NMX;
+            cs[k][m] = m < nm ? (float)E.coeffs[((size_t)t * E.n_real + r0 + k) * nm + m] : 0.f;
         }
         __syncthreads();
         if (!ok) continue;
-        for (int k = 0; k < n; ++k) {
-            float vx = mx32, vy = my32;
+        // two realizations per step; (vx, vy) in one packed FFMA2 chain.
+        // Unused modes hold zeros (exact no-ops), so no mode-count test.
+        // chunks hold an even count except possibly the last (n odd: the
+        // second lane of the pair re-evaluates realization k, harmless)
+        for (int k = 0; k < n; k += 2) {
+            const int k1 = k + 1 < n ? k + 1 : k;
+            float2 v0 = make_float2(mx32, my32), v1 = v0;
 #pragma unroll
-            for (int m = 0; m < NMX; ++m)
-                if (m < nm) {
-                    const float cc = cs[k][m];
-                    vx = fmaf(cc, dx32[m], vx);
-                    vy = fmaf(cc, dy32[m], vy);
-                }
-            if (fabsf(vx) >= thx) {
-                ex = fmax(ex, vmax_exact_component<NMX>(G, E, t, r0 + k, c, 0));
-                thx = __double2float_rd(ex - delx);
+            for (int m = 0; m < NMX; ++m) {
+                v0 = ffma2_bcast(cs[k][m], d32[m], v0);
+                v1 = ffma2_bcast(cs[k1][m], d32[m], v1);
             }
-            if (fabsf(vy) >= thy) {
-                ey = fmax(ey, vmax_exact_component<NMX>(G, E, t, r0 + k, c, 1));
-                thy = __double2float_rd(ey - dely);
+            // !(|v| < th) also routes NaN / inf to the exact path
+            const bool hit = !(fabsf(v0.x) < thx) || !(fabsf(v0.y) < thy) || !(fabsf(v1.x) < thx) ||
+                             !(fabsf(v1.y) < thy);
+            if (hit) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const float2 v = j ? v1 : v0;
+                    const int r = r0 + (j ? k1 : k);
+                    if (!(fabsf(v.x) < thx)) {
+                        const double e = vmax_exact_component<NMX>(G, E, t, r, c, 0);
+                        ex = (e != e || e > ex) ? e : ex;   // NaN sticks (the reference's max propagates it)
+                        thx = __double2float_rd(ex - delx);
+                    }
+                    if (!(fabsf(v.y) < thy)) {
+                        const double e = vmax_exact_component<NMX>(G, E, t, r, c, 1);
+                        ey = (e != e || e > ey) ? e : ey;
+                        thy = __double2float_rd(ey - dely);
+                    }
+                }
             }
         }
     }
-    ex = warp_max_f64(ex);
-    ey = warp_max_f64(ey);
+    // non-negative doubles (and +NaN, above +inf) order like their bit patterns
+    unsigned long long bx = (unsigned long long)__double_as_longlong(ex),
+                       by = (unsigned long long)__double_as_longlong(ey);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long ox = __shfl_xor_sync(kFull, bx, o), oy = __shfl_xor_sync(kFull, by, o);
+        bx = ox > bx ? ox : bx;
+        by = oy > by ? oy : by;
+    }
+    ex = __longlong_as_double((long long)bx);
+    ey = __longlong_as_double((long long)by);
     if ((threadIdx.x & 31) == 0) {
         atomic_max_nonneg(out2, ex);
         atomic_max_nonneg(out2 + 1, ey);
@@ -230,6 +287,7 @@ extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *st
     if (G.nx < 1 || G.ny < 1 || G.nt < 1 || E.n_real < 1 || E.n_modes < 0 || E.n_modes > 16)
         return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims (n_modes must be <= 16)");
     cudaStream_t s = (cudaStream_t)stream;
+    pool_keep();
     const int nc = G.nx * G.ny;
     const int nm = E.n_modes;
     // max_r |coeff[t, r, m]| per (t, m): the error-bound ingredient
@@ -856,8 +914,9 @@ template <int FLAGS>
 #ifndef FM_BUILD_RC
 #define FM_BUILD_RC 64
 #endif
-__global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, const BuildK *__restrict__ Kg)
+__global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_constant__ BuildK K)
 {
+    const BuildK *__restrict__ Kg = &K;   // the parameter block, for the noinline rare paths
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *wbase = smem + (size_t)warp * K.smem_warp;
@@ -1171,10 +1230,9 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const BuildK K, co
 // Recomputes one (t, a) sweep over every (r, c) of the layer to reproduce
 // the reference's ContractViolation message (model_builder.py:430-438):
 // argmax over non-sink entries of |di|+|dj|, first flat index r*N_c + c.
-__global__ void k_viol_report(const BuildK *__restrict__ Kg, int t, int a, int pass, unsigned long long *best,
+__global__ void k_viol_report(const __grid_constant__ BuildK K, int t, int a, int pass, unsigned long long *best,
                               int32_t *didj)
 {
-    const BuildK &K = *Kg;
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (long long)K.nr * K.nc) return;
     const int r = (int)(idx / K.nc), c = (int)(idx % K.nc);
@@ -1211,19 +1269,19 @@ __global__ void k_viol_report(const BuildK *__restrict__ Kg, int t, int a, int p
 }
 
 template <int FL>
-static int32_t launch_build_t(const BuildK &K, const BuildK *Kg, size_t smem, cudaStream_t s)
+static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
 {
     auto kern = k_build<FL>;
     FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));
     if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", smem);
-    kern<<<occ * sm_count(), 128, smem, s>>>(K, Kg);
+    kern<<<occ * sm_count(), 128, smem, s>>>(K);
     FM_CK_LAUNCH("k_build");
     return FM_OK;
 }
 
-static int32_t launch_build(const BuildK &K, const BuildK *Kg, int flags, size_t smem, cudaStream_t s)
+static int32_t launch_build(const BuildK &K, int flags, size_t smem, cudaStream_t s)
 {
     if (flags & F_PROVEN) {
         // lean variants exist for the identity geometry (dt = dx = 1, origin
@@ -1232,7 +1290,7 @@ static int32_t launch_build(const BuildK &K, const BuildK *Kg, int flags, size_t
         const int geo = (flags & 15) == (F_DT_ONE | F_OX_ZERO | F_DX_ONE) ? (flags & 15) : 0;
         switch (geo | (flags & (F_NET | F_PROVEN | F_CNT))) {
 #define FM_CASE(F) \
-    case F: return launch_build_t<F>(K, Kg, smem, s);
+    case F: return launch_build_t<F>(K, smem, s);
             FM_CASE(11 | F_PROVEN) FM_CASE(11 | F_PROVEN | F_CNT) FM_CASE(11 | F_PROVEN | F_NET)
             FM_CASE(F_PROVEN) FM_CASE(F_PROVEN | F_CNT) FM_CASE(F_PROVEN | F_NET)
 #undef FM_CASE
@@ -1241,7 +1299,7 @@ static int32_t launch_build(const BuildK &K, const BuildK *Kg, int flags, size_t
     }
     switch (flags) {
 #define FM_CASE(F) \
-    case F: return launch_build_t<F>(K, Kg, smem, s);
+    case F: return launch_build_t<F>(K, smem, s);
         FM_CASE(0) FM_CASE(1) FM_CASE(2) FM_CASE(3) FM_CASE(4) FM_CASE(5) FM_CASE(6) FM_CASE(7)
         FM_CASE(8) FM_CASE(9) FM_CASE(10) FM_CASE(11) FM_CASE(16) FM_CASE(17) FM_CASE(18) FM_CASE(19)
         FM_CASE(20) FM_CASE(21) FM_CASE(22) FM_CASE(23) FM_CASE(24) FM_CASE(25) FM_CASE(26) FM_CASE(27)
@@ -1407,14 +1465,8 @@ extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *st
     int flags = 0;
     int32_t st = build_params(h, M, K, flags);
     if (st != FM_OK) return st;
-    BuildK *Kg = nullptr;
-    FM_CK(cudaMallocAsync(&Kg, sizeof(BuildK), s));
-    FM_CK(cudaMemcpyAsync(Kg, &K, sizeof(BuildK), cudaMemcpyHostToDevice, s));
     FM_CK(cudaMemsetAsync(h->task_counter, 0, sizeof(unsigned int), s));
-    st = launch_build(K, Kg, flags, (size_t)4 * K.smem_warp, s);
-    if (st != FM_OK) return st;
-    FM_CK(cudaFreeAsync(Kg, s));
-    return FM_OK;
+    return launch_build(K, flags, (size_t)4 * K.smem_warp, s);
 }
 
 extern "C" int32_t fm_build_check(const fm_build_args *h, fm_model *M, uint64_t *h_needed, fm_violation *h_viol,
@@ -1437,22 +1489,18 @@ extern "C" int32_t fm_build_check(const fm_build_args *h, fm_model *M, uint64_t 
         for (int a = 0; a < h->n_actions; ++a) {
             if (!flags_h[(size_t)t * h->n_actions + a]) continue;
             // reproduce the reference message for the first (t, a)
-            BuildK *Kg = nullptr;
             unsigned long long *d_best;
-            FM_CK(cudaMallocAsync(&Kg, sizeof(BuildK), s));
-            FM_CK(cudaMemcpyAsync(Kg, &K, sizeof(BuildK), cudaMemcpyHostToDevice, s));
             FM_CK(cudaMallocAsync(&d_best, sizeof(unsigned long long) + 2 * sizeof(int32_t), s));
             int32_t *d_didj = reinterpret_cast<int32_t *>(d_best + 1);
             FM_CK(cudaMemsetAsync(d_best, 0, sizeof(unsigned long long) + 2 * sizeof(int32_t), s));
             const long long n = (long long)K.nr * K.nc;
             const unsigned nb = (unsigned)((n + 255) / 256);
-            k_viol_report<<<nb, 256, 0, s>>>(Kg, t, a, 0, d_best, d_didj);
-            k_viol_report<<<nb, 256, 0, s>>>(Kg, t, a, 1, d_best, d_didj);
+            k_viol_report<<<nb, 256, 0, s>>>(K, t, a, 0, d_best, d_didj);
+            k_viol_report<<<nb, 256, 0, s>>>(K, t, a, 1, d_best, d_didj);
             FM_CK_LAUNCH_N("k_viol_report", 2);
             int32_t didj[2] = {0, 0};
             FM_CK(cudaMemcpyAsync(didj, d_didj, sizeof(didj), cudaMemcpyDeviceToHost, s));
             FM_CK(cudaFreeAsync(d_best, s));
-            FM_CK(cudaFreeAsync(Kg, s));
             FM_CK(cudaStreamSynchronize(s));
             if (h_viol) {
                 h_viol->t = t; h_viol->a = a; h_viol->di = didj[0]; h_viol->dj = didj[1];

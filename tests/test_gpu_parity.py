@@ -313,3 +313,20 @@ def test_planner_deferred_check_and_capacity_retry():
     plan = fm.plan(env, acts, rcfg, target)
     if res == 0.0:
         assert plan.values.cpu().numpy().tobytes() == ov.tobytes()
+
+
+def test_model_buffer_reuse():
+    """A build into the buffers of a previous model (reuse=) equals a fresh build."""
+    env, acts, rcfg, target = make_random_env(7005)
+    de = DeviceEnv.from_host(env)
+    sub = fm.compute_subgrid(env.field, acts, env.grid, device_env=de)
+    om = O.build_model(env, acts, rcfg, target, sub.half_width_x, sub.half_width_y)
+    first = build_device_model(de, acts, rcfg, target, sub)
+    other = RewardConfig("net_energy", c_f=1.0, c_r=0.7, r_term=10.0, r_outbound=-60.0)
+    second = build_device_model(de, acts, other, target, sub, reuse=first)
+    third = build_device_model(de, acts, rcfg, target, sub, reuse=second)
+    assert model_digest(third.to_sparse_model()) == model_digest(om)
+    part = build_device_model(de, acts, rcfg, target, sub, j_range=(1, 3), reuse=third)
+    fresh = build_device_model(de, acts, rcfg, target, sub, j_range=(1, 3))
+    import torch
+    assert torch.equal(part.row_nnz, fresh.row_nnz) and torch.equal(part.reward, fresh.reward)
