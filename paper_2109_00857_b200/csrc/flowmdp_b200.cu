@@ -652,8 +652,8 @@ __device__ __forceinline__ int floor_magic(double u)
 // overridden here; everything else goes to rare_transition.
 template <int FLAGS, bool EDGE, bool OBST>
 __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, const double2 v,
-                                                const double *__restrict__ g_n, const uint32_t *dang, int outq,
-                                                int &q, double &rw)
+                                                const double *__restrict__ g_n, const uint32_t *dang,
+                                                const uint32_t *dseg, int outq, int &q, double &rw)
 {
     double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
     if (!(FLAGS & F_DT_ONE)) {
@@ -686,9 +686,23 @@ __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, 
     bool ok = inwin;
     if (OBST) {
         const int slot = q + R.soff;
-        const bool dz = inwin && ((dang[slot >> 5] >> (slot & 31)) & 1u);
+        const unsigned bit = 1u << (slot & 31);
+        // landing cell masked at t+1: bad whatever the transit (model_builder.py:336, 347)
+#ifdef FM_NO_LAND_INLINE
+        const bool land = false;
+        (void)dseg;
+        const bool segd = inwin && ((dang[slot >> 5] | dseg[slot >> 5]) & bit);
+#else
+        const bool land = inwin && (dang[slot >> 5] & bit);
+        // gated segment whose box touches the mask at t: exact test needed
+        const bool segd = inwin && !land && (dseg[slot >> 5] & bit);
+#endif
         const bool dead = R.rflags & RF_DEAD;
-        ok = inwin && (!dz || dead);
+        ok = inwin && (!segd || dead);
+        if (land) {
+            q = outq;
+            rw = K.r_out;
+        }
         if (dead) {   // after the overflow check (model_builder.py:445-452)
             q = outq;
             rw = (R.rflags & RF_TERMINAL) ? 0.0 : K.r_out;
@@ -853,18 +867,18 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
 template <int FLAGS, bool EDGE, bool OBST>
 __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
                                            const double2 *vrow, int nk, const double *__restrict__ g_n,
-                                           const uint32_t *dang, uint16_t *h16q, int outq, unsigned rowmask,
-                                           double &S, int &viol)
+                                           const uint32_t *dang, const uint32_t *dseg, uint16_t *h16q, int outq,
+                                           unsigned rowmask, double &S, int &viol)
 {
     int k = 0;
     for (; k + 4 <= nk; k += 4) {
         const double2 v0 = vrow[k], v1 = vrow[k + 1], v2 = vrow[k + 2], v3 = vrow[k + 3];
         int q0, q1, q2, q3;
         double w0, w1, w2, w3;
-        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, v0, g_n, dang, outq, q0, w0);
-        const bool f1 = fast_transition<FLAGS, EDGE, OBST>(K, R, v1, g_n, dang, outq, q1, w1);
-        const bool f2 = fast_transition<FLAGS, EDGE, OBST>(K, R, v2, g_n, dang, outq, q2, w2);
-        const bool f3 = fast_transition<FLAGS, EDGE, OBST>(K, R, v3, g_n, dang, outq, q3, w3);
+        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, v0, g_n, dang, dseg, outq, q0, w0);
+        const bool f1 = fast_transition<FLAGS, EDGE, OBST>(K, R, v1, g_n, dang, dseg, outq, q1, w1);
+        const bool f2 = fast_transition<FLAGS, EDGE, OBST>(K, R, v2, g_n, dang, dseg, outq, q2, w2);
+        const bool f3 = fast_transition<FLAGS, EDGE, OBST>(K, R, v3, g_n, dang, dseg, outq, q3, w3);
         if (!__all_sync(rowmask, f0 && f1 && f2 && f3)) {
             if (!f0) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v0); q0 = o.slot; w0 = o.rw; viol |= o.viol; }
             if (!f1) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v1); q1 = o.slot; w1 = o.rw; viol |= o.viol; }
@@ -883,7 +897,7 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
     for (; k < nk; ++k) {
         int q0;
         double w0;
-        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, vrow[k], g_n, dang, outq, q0, w0);
+        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, vrow[k], g_n, dang, dseg, outq, q0, w0);
         if (!f0) {
             const SlowOut o = rare_transition<FLAGS>(Kg, t, R, vrow[k]);
             q0 = o.slot;
@@ -907,13 +921,20 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
 //                      by all AG row lanes of that cell.  Coefficients of the
 //                      next chunk stream in with cp.async while the row lanes
 //                      work on the current one.
-template <int FLAGS>
+//
+// PART splits the tasks by warp class so each launch carries only the code
+// its warps run (the full kernel's instruction footprint thrashes the
+// instruction cache: ncu "no instruction" stalls):
+//   0 all tasks, 1 tasks without obstacle / dead rows (lean code only),
+//   2 the rest.  Both parts classify every task the same way and skip the
+//   other part's tasks.
 #ifndef FM_BUILD_MINB
 #define FM_BUILD_MINB 4
 #endif
 #ifndef FM_BUILD_RC
 #define FM_BUILD_RC 64
 #endif
+template <int FLAGS, int PART>
 __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_constant__ BuildK K)
 {
     const BuildK *__restrict__ Kg = &K;   // the parameter block, for the noinline rare paths
@@ -1012,6 +1033,11 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                                          R.cj + K.hy >= K.ny);
         double S = 0.0;
         int viol = 0;
+        if (PART != 0) {
+            const bool obst_task =
+                !horizon && __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
+            if (obst_task != (PART == 2)) continue;   // the other launch's task
+        }
 
         if (horizon) {
             // step_flat's horizon branch (model_builder.py:319-328): every
@@ -1024,31 +1050,37 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
         } else {
             const bool edge = __any_sync(kFull, edge_row);
             const unsigned rowmask = __ballot_sync(kFull, row_ok);   // lanes that run chunk_rows
-            const bool obst = __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
+            const bool obst = PART == 1   ? false
+                              : PART == 2 ? true
+                                          : __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
             const int DW = (nslot + 31) >> 5;
             if (obst) {
-                // danger[cs][slot]: landing cell masked at t+1, or (gated cell)
-                // the segment box [min(c,l)-1, max(c,l)+1] touches the mask at t
+                // danger[0][cs][slot]: landing cell masked at t+1 (bad, settled
+                // inline); danger[1][cs][slot]: (gated cell) the segment box
+                // [min(c,l)-1, max(c,l)+1] touches the mask at t (exact test)
                 for (int wd = 0; wd < CW * DW; ++wd) {
                     const int cs = wd / DW, sl = (wd - cs * DW) * 32 + lane;
                     const int lc = grp * CW + cs;
-                    bool bit = false;
+                    bool land = false, seg = false;
                     if (lc < K.ncell && sl < nslot) {
                         const int cc = K.cell0 + lc, cci = cc % K.nx, ccj = cc / K.nx;
                         const int li = cci + sl % W - K.hx, lj = ccj + sl / W - K.hy;
                         if ((unsigned)li < (unsigned)K.nx && (unsigned)lj < (unsigned)K.ny) {
-                            bit = K.mask[(size_t)(t + 1) * K.nc + lj * K.nx + li] != 0;
-                            if (!bit && box_count(K, t, cci - rx, cci + rx, ccj - ry, ccj + ry) > 0)
-                                bit = box_count(K, t, min(cci, li) - 1, max(cci, li) + 1, min(ccj, lj) - 1,
+                            land = K.mask[(size_t)(t + 1) * K.nc + lj * K.nx + li] != 0;
+                            if (!land && box_count(K, t, cci - rx, cci + rx, ccj - ry, ccj + ry) > 0)
+                                seg = box_count(K, t, min(cci, li) - 1, max(cci, li) + 1, min(ccj, lj) - 1,
                                                 max(ccj, lj) + 1) > 0;
                         }
                     }
-                    const unsigned word = __ballot_sync(kFull, bit);
-                    if (lane == 0) danger[wd] = word;
+                    const unsigned wl = __ballot_sync(kFull, land), ws = __ballot_sync(kFull, seg);
+                    if (lane == 0) {
+                        danger[wd] = wl;
+                        danger[CW * DW + wd] = ws;
+                    }
                 }
                 __syncwarp();
             }
-            const uint32_t *dang = danger + cs_row * DW;
+            const uint32_t *dang = danger + cs_row * DW, *dseg = danger + (CW + cs_row) * DW;
             // fast-path form of the row constants: target slot and OUT slot in
             // q = slot - soff coordinates, histogram pointer shifted by soff
             RowC Rf = R;
@@ -1159,26 +1191,52 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                     FM_STAT(obst ? 3 : 4, nk);
                     if (obst) {
                         if (edge)
-                            chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, h16q, outq, rowmask, S,
                                                           viol);
                         else
-                            chunk_rows<FLAGS, false, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, false, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, h16q, outq, rowmask, S,
                                                            viol);
                     } else if (FLAGS & F_PROVEN) {
+                        // F_CNT: edge rows count out-of-domain landings in their
+                        // (unclipped) window slots and fold them into OUT below
+#ifdef FM_NO_EDGE_FOLD
                         if (edge)
+#else
+                        if (edge && !(FLAGS & F_CNT))
+#endif
                             chunk_rows_lean<FLAGS, true>(K, Rf, vrow, nk, g_n, h16q, outq, S, half_one);
                         else
                             chunk_rows_lean<FLAGS, false>(K, Rf, vrow, nk, g_n, h16q, outq, S, half_one);
                     } else {
                         if (edge)
-                            chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, h16q, outq, rowmask, S,
                                                            viol);
                         else
-                            chunk_rows<FLAGS, false, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, h16q, outq, rowmask,
+                            chunk_rows<FLAGS, false, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, h16q, outq, rowmask,
                                                             S, viol);
                     }
                 }
                 __syncwarp();
+            }
+#ifdef FM_NO_EDGE_FOLD
+            if (false) {
+#else
+            if ((FLAGS & F_CNT) && !obst && row_ok && edge_row) {
+#endif
+                // window slots whose cell lies outside the domain held the
+                // landings that leave it: SINK (model_builder.py:331-335, 347)
+                int extra = 0;
+                for (int dj = -K.hy; dj <= K.hy; ++dj) {
+                    const bool jout = (unsigned)(R.cj + dj) >= (unsigned)K.ny;
+                    for (int di = -K.hx; di <= K.hx; ++di) {
+                        if (jout || (unsigned)(R.ci + di) >= (unsigned)K.nx) {
+                            uint16_t &cnt = h16[((dj + K.hy) * W + di + K.hx) * 32];
+                            extra += cnt;
+                            cnt = 0;
+                        }
+                    }
+                }
+                h16[nslot * 32] += (uint16_t)extra;
             }
             if ((FLAGS & F_CNT) && !obst && row_ok) {
                 // exact reward sum from the counts (F_CNT): every partial sum
@@ -1268,17 +1326,30 @@ __global__ void k_viol_report(const __grid_constant__ BuildK K, int t, int a, in
     }
 }
 
-template <int FL>
-static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
+template <int FL, int PART>
+static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
 {
-    auto kern = k_build<FL>;
+    auto kern = k_build<FL, PART>;
     FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));
     if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", smem);
+    FM_CK(cudaMemsetAsync(K.task_counter, 0, sizeof(unsigned int), s));
     kern<<<occ * sm_count(), 128, smem, s>>>(K);
     FM_CK_LAUNCH("k_build");
     return FM_OK;
+}
+
+template <int FL>
+static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
+{
+    if constexpr (!(FL & F_PROVEN)) {
+        return launch_build_p<FL, 0>(K, smem, s);
+    } else {
+        const int32_t st = launch_build_p<FL, 1>(K, smem, s);
+        if (st != FM_OK) return st;
+        return launch_build_p<FL, 2>(K, smem, s);
+    }
 }
 
 static int32_t launch_build(const BuildK &K, int flags, size_t smem, cudaStream_t s)
@@ -1437,7 +1508,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.off_coef = K.off_vbuf + K.CW * (K.RC + 1) * (int)sizeof(double2);
     K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
     K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
-    K.smem_warp = align16(K.off_danger + K.CW * (int)((nslot + 31) / 32) * 4);
+    K.smem_warp = align16(K.off_danger + 2 * K.CW * (int)((nslot + 31) / 32) * 4);
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
     K.entries = M->entries; K.capacity = M->capacity;
     K.nnz_counter = reinterpret_cast<unsigned long long *>(M->d_nnz);
