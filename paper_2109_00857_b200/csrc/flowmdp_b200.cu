@@ -416,6 +416,7 @@ struct BuildK {
     // sub-grid
     int hx, hy, width, nslot, hw;
     int rx, ry;
+    int src_cell_exact;      // floor((x0(c) - o) / dx) == c for every cell centre
     const int32_t *gate_r;   // device [rx, ry] (fm_gate_radius) or null
     // task decomposition
     int t0, t1, cell0, ncell;   // strip = cells [cell0, cell0 + ncell) of each layer
@@ -653,7 +654,8 @@ __device__ __forceinline__ int floor_magic(double u)
 template <int FLAGS, bool EDGE, bool OBST>
 __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, const double2 v,
                                                 const double *__restrict__ g_n, const uint32_t *dang,
-                                                const uint32_t *dseg, int outq, int &q, double &rw)
+                                                const uint32_t *dseg, const uint32_t *dloose, int outq, int &q,
+                                                double &rw)
 {
     double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
     if (!(FLAGS & F_DT_ONE)) {
@@ -691,11 +693,23 @@ __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, 
 #ifdef FM_NO_LAND_INLINE
         const bool land = false;
         (void)dseg;
-        const bool segd = inwin && ((dang[slot >> 5] | dseg[slot >> 5]) & bit);
+        const bool segd = inwin && ((dang[slot >> 5] | dloose[slot >> 5]) & bit);
 #else
         const bool land = inwin && (dang[slot >> 5] & bit);
         // gated segment whose box touches the mask at t: exact test needed
-        const bool segd = inwin && !land && (dseg[slot >> 5] & bit);
+        // gated segment: its sample cells lie in the box spanned by the source
+        // cell and the cell of ex = x0 + (x1 - x0) (seg_blocked); `tight` =
+        // that box with ex's cell = the landing cell touches the mask at t,
+        // `loose` = the same box grown by one cell (covers any ex)
+        const bool tight = inwin && !land && (dseg[slot >> 5] & bit);
+        const bool loose = inwin && !land && (dloose[slot >> 5] & bit);
+        bool segd = tight;
+        if (loose && !tight) {   // blocked only if ex leaves the landing cell
+            const double ex = DADD(R.x0, DSUB(x1, R.x0)), ey = DADD(R.y0, DSUB(y1, R.y0));
+            const int ei = __double2int_rd(to_cell<FLAGS>(ex, K.ox, K.dx, K.inv_dx));
+            const int ej = __double2int_rd(to_cell<FLAGS>(ey, K.oy, K.dx, K.inv_dx));
+            segd = ei != i1 || ej != j1;
+        }
 #endif
         const bool dead = R.rflags & RF_DEAD;
         ok = inwin && (!segd || dead);
@@ -867,7 +881,8 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
 template <int FLAGS, bool EDGE, bool OBST>
 __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
                                            const double2 *vrow, int nk, const double *__restrict__ g_n,
-                                           const uint32_t *dang, const uint32_t *dseg, uint16_t *h16q, int outq,
+                                           const uint32_t *dang, const uint32_t *dseg, const uint32_t *dloose,
+                                           uint16_t *h16q, int outq,
                                            unsigned rowmask, double &S, int &viol)
 {
     int k = 0;
@@ -875,10 +890,10 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
         const double2 v0 = vrow[k], v1 = vrow[k + 1], v2 = vrow[k + 2], v3 = vrow[k + 3];
         int q0, q1, q2, q3;
         double w0, w1, w2, w3;
-        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, v0, g_n, dang, dseg, outq, q0, w0);
-        const bool f1 = fast_transition<FLAGS, EDGE, OBST>(K, R, v1, g_n, dang, dseg, outq, q1, w1);
-        const bool f2 = fast_transition<FLAGS, EDGE, OBST>(K, R, v2, g_n, dang, dseg, outq, q2, w2);
-        const bool f3 = fast_transition<FLAGS, EDGE, OBST>(K, R, v3, g_n, dang, dseg, outq, q3, w3);
+        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, v0, g_n, dang, dseg, dloose, outq, q0, w0);
+        const bool f1 = fast_transition<FLAGS, EDGE, OBST>(K, R, v1, g_n, dang, dseg, dloose, outq, q1, w1);
+        const bool f2 = fast_transition<FLAGS, EDGE, OBST>(K, R, v2, g_n, dang, dseg, dloose, outq, q2, w2);
+        const bool f3 = fast_transition<FLAGS, EDGE, OBST>(K, R, v3, g_n, dang, dseg, dloose, outq, q3, w3);
         if (!__all_sync(rowmask, f0 && f1 && f2 && f3)) {
             if (!f0) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v0); q0 = o.slot; w0 = o.rw; viol |= o.viol; }
             if (!f1) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v1); q1 = o.slot; w1 = o.rw; viol |= o.viol; }
@@ -897,7 +912,7 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
     for (; k < nk; ++k) {
         int q0;
         double w0;
-        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, vrow[k], g_n, dang, dseg, outq, q0, w0);
+        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, vrow[k], g_n, dang, dseg, dloose, outq, q0, w0);
         if (!f0) {
             const SlowOut o = rare_transition<FLAGS>(Kg, t, R, vrow[k]);
             q0 = o.slot;
@@ -1061,26 +1076,34 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                 for (int wd = 0; wd < CW * DW; ++wd) {
                     const int cs = wd / DW, sl = (wd - cs * DW) * 32 + lane;
                     const int lc = grp * CW + cs;
-                    bool land = false, seg = false;
+                    bool land = false, tight = false, loose = false;
                     if (lc < K.ncell && sl < nslot) {
                         const int cc = K.cell0 + lc, cci = cc % K.nx, ccj = cc / K.nx;
                         const int li = cci + sl % W - K.hx, lj = ccj + sl / W - K.hy;
                         if ((unsigned)li < (unsigned)K.nx && (unsigned)lj < (unsigned)K.ny) {
                             land = K.mask[(size_t)(t + 1) * K.nc + lj * K.nx + li] != 0;
-                            if (!land && box_count(K, t, cci - rx, cci + rx, ccj - ry, ccj + ry) > 0)
-                                seg = box_count(K, t, min(cci, li) - 1, max(cci, li) + 1, min(ccj, lj) - 1,
-                                                max(ccj, lj) + 1) > 0;
+                            if (!land && box_count(K, t, cci - rx, cci + rx, ccj - ry, ccj + ry) > 0) {
+                                loose = box_count(K, t, min(cci, li) - 1, max(cci, li) + 1, min(ccj, lj) - 1,
+                                                  max(ccj, lj) + 1) > 0;
+                                // tight needs cell(x0) == source cell (host-checked)
+                                tight = loose && (!K.src_cell_exact ||
+                                                  box_count(K, t, min(cci, li), max(cci, li), min(ccj, lj),
+                                                            max(ccj, lj)) > 0);
+                            }
                         }
                     }
-                    const unsigned wl = __ballot_sync(kFull, land), ws = __ballot_sync(kFull, seg);
+                    const unsigned wl = __ballot_sync(kFull, land), wt = __ballot_sync(kFull, tight),
+                                   wo = __ballot_sync(kFull, loose);
                     if (lane == 0) {
                         danger[wd] = wl;
-                        danger[CW * DW + wd] = ws;
+                        danger[CW * DW + wd] = wt;
+                        danger[2 * CW * DW + wd] = wo;
                     }
                 }
                 __syncwarp();
             }
-            const uint32_t *dang = danger + cs_row * DW, *dseg = danger + (CW + cs_row) * DW;
+            const uint32_t *dang = danger + cs_row * DW, *dseg = danger + (CW + cs_row) * DW,
+                           *dloose = danger + (2 * CW + cs_row) * DW;
             // fast-path form of the row constants: target slot and OUT slot in
             // q = slot - soff coordinates, histogram pointer shifted by soff
             RowC Rf = R;
@@ -1191,10 +1214,10 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                     FM_STAT(obst ? 3 : 4, nk);
                     if (obst) {
                         if (edge)
-                            chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, dloose, h16q, outq, rowmask, S,
                                                           viol);
                         else
-                            chunk_rows<FLAGS, false, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, false, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, dloose, h16q, outq, rowmask, S,
                                                            viol);
                     } else if (FLAGS & F_PROVEN) {
                         // F_CNT: edge rows count out-of-domain landings in their
@@ -1209,10 +1232,10 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                             chunk_rows_lean<FLAGS, false>(K, Rf, vrow, nk, g_n, h16q, outq, S, half_one);
                     } else {
                         if (edge)
-                            chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, dloose, h16q, outq, rowmask, S,
                                                            viol);
                         else
-                            chunk_rows<FLAGS, false, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, h16q, outq, rowmask,
+                            chunk_rows<FLAGS, false, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, dloose, h16q, outq, rowmask,
                                                             S, viol);
                     }
                 }
@@ -1406,6 +1429,17 @@ static bool prove_axis(int n, double o, double dx, double reach, int hw)
     return true;
 }
 
+// Every cell centre x0 = o + (c + 0.5) dx maps back to its own cell under
+// the reference's (x - o) / dx and floor (environment.py:99-100, 358-362).
+static bool source_cells_exact(const fm_grid &G)
+{
+    for (int c = 0; c < (G.nx > G.ny ? G.nx : G.ny); ++c) {
+        if (c < G.nx && floor(((G.ox + ((double)c + 0.5) * G.dx) - G.ox) / G.dx) != c) return false;
+        if (c < G.ny && floor(((G.oy + ((double)c + 0.5) * G.dx) - G.oy) / G.dx) != c) return false;
+    }
+    return true;
+}
+
 static bool prove_lean(const fm_build_args *h)
 {
     const double vx = h->vmax_x, vy = h->vmax_y;
@@ -1508,7 +1542,8 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.off_coef = K.off_vbuf + K.CW * (K.RC + 1) * (int)sizeof(double2);
     K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
     K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
-    K.smem_warp = align16(K.off_danger + 2 * K.CW * (int)((nslot + 31) / 32) * 4);
+    K.smem_warp = align16(K.off_danger + 3 * K.CW * (int)((nslot + 31) / 32) * 4);
+    K.src_cell_exact = source_cells_exact(G) ? 1 : 0;
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
     K.entries = M->entries; K.capacity = M->capacity;
     K.nnz_counter = reinterpret_cast<unsigned long long *>(M->d_nnz);
