@@ -191,6 +191,44 @@ int32_t fm_export_coo(const fm_model *h_model, uint64_t *d_scratch,
                       uint64_t *d_block_off, uint32_t *rows, uint32_t *cols,
                       double *vals, double *rewards, void *stream);
 
+/* Model file image (io.write_model, io.py:213-244) from the fm_export_coo
+ * arrays: per (action, time) block rows u32, cols u32, vals f32, then the
+ * f32 rewards, written at byte `header_bytes` of d_img (the caller writes
+ * the header: magic, version/n_states/n_actions/nt, nnz, block offsets). */
+int32_t fm_model_image(const uint64_t *d_block_off, int32_t n_blocks,
+                       const uint32_t *rows, const uint32_t *cols, const double *vals,
+                       uint64_t nnz, const double *rewards, uint64_t n_rewards,
+                       uint64_t header_bytes, unsigned char *d_img, void *stream);
+
+/* ---- rollout ------------------------------------------------------------ */
+/* Ensemble rollout (rollout.py:107-208): trajectory k follows the policy in
+ * realization realizations[k] from the start cell, one step_flat per time
+ * index (model_builder.py:286-369).  Row s of trajectory k (s < n_rows[k])
+ * is (departure cell, action, cause code CAUSE_*, reward, cumulative
+ * reward) at [k * max_rows + s]; final_cell[k] = arrival cell when the last
+ * row reached the target, else -1.  The start cell must not be masked at
+ * t = 0 (the caller handles that case, rollout.py:124-136). */
+typedef struct {
+    fm_grid grid;
+    fm_env env;
+    fm_reward reward;
+    const fm_action *actions; /* device [n_actions] */
+    int32_t n_actions;
+    const int32_t *mask_sat;  /* device, fm_mask_sat */
+    const int32_t *d_gate_r;  /* device [rx, ry], fm_gate_radius */
+    const uint16_t *policy;   /* device [N_g] */
+    int32_t start_i, start_j;
+    const int32_t *realizations; /* device [n_traj] */
+    int32_t n_traj, max_rows;    /* max_rows >= nt */
+    int32_t *row_cell;
+    int16_t *row_action;
+    int8_t *row_cause;
+    double *row_reward, *row_cum;
+    int32_t *n_rows, *final_cell;
+} fm_rollout_args;
+
+int32_t fm_rollout(const fm_rollout_args *h_args, void *stream);
+
 /* ---- solve -------------------------------------------------------------- */
 /* Backward-in-time Bellman sweep over the compact model, layers
  * t = t_hi-1 .. t_lo (value_iteration's fixed point, solver.py:75-109,

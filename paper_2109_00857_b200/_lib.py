@@ -104,6 +104,17 @@ class FmCsr(C.Structure):
                 ("rewards", C.c_void_p)]
 
 
+class FmRolloutArgs(C.Structure):
+    _fields_ = [("grid", FmGrid), ("env", FmEnv), ("reward", FmReward),
+                ("actions", C.c_void_p), ("n_actions", C.c_int32),
+                ("mask_sat", C.c_void_p), ("d_gate_r", C.c_void_p), ("policy", C.c_void_p),
+                ("start_i", C.c_int32), ("start_j", C.c_int32),
+                ("realizations", C.c_void_p), ("n_traj", C.c_int32), ("max_rows", C.c_int32),
+                ("row_cell", C.c_void_p), ("row_action", C.c_void_p), ("row_cause", C.c_void_p),
+                ("row_reward", C.c_void_p), ("row_cum", C.c_void_p),
+                ("n_rows", C.c_void_p), ("final_cell", C.c_void_p)]
+
+
 # exported symbols and their signatures; tests check every one resolves
 SIGNATURES = {
     "fm_abi_version": (C.c_int32, []),
@@ -134,6 +145,9 @@ SIGNATURES = {
     "fm_policy_value": (C.c_int32, [C.POINTER(FmCsr), C.c_void_p, C.c_double, C.c_int32, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p]),
     "fm_fp64_probe": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "fm_model_image": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                   C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "fm_rollout": (C.c_int32, [C.POINTER(FmRolloutArgs), C.c_void_p]),
 }
 
 _LIB = None

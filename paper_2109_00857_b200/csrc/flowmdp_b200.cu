@@ -2172,3 +2172,172 @@ extern "C" int32_t fm_fp64_probe(double *d_sink, int32_t blocks, int32_t iters, 
     FM_CK_LAUNCH("k_fp64_probe");
     return FM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Model file image (io.write_model, io.py:213-244): after fm_export_coo the
+// canonical COO sits in block order; one thread per entry writes its row,
+// column and f32 probability into the block's three arrays, and one thread
+// per (action, state) writes the f32 reward.  The caller writes the header
+// (magic, version, sizes, block offsets) in front: `header` bytes.
+// ---------------------------------------------------------------------------
+__global__ void k_model_image(const uint64_t *block_off, int n_blocks, const uint32_t *rows, const uint32_t *cols,
+                              const double *vals, uint64_t nnz, const double *rewards, uint64_t n_rew,
+                              uint64_t header, unsigned char *img)
+{
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < nnz) {
+        int lo = 0, hi = n_blocks - 1;   // block of entry e: last k with block_off[k] <= e
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (block_off[mid] <= e) lo = mid;
+            else hi = mid - 1;
+        }
+        const uint64_t b0 = block_off[lo], n = block_off[lo + 1] - b0, i = e - b0;
+        unsigned char *base = img + header + 12 * b0;
+        reinterpret_cast<uint32_t *>(base)[i] = rows[e];
+        reinterpret_cast<uint32_t *>(base + 4 * n)[i] = cols[e];
+        reinterpret_cast<float *>(base + 8 * n)[i] = __double2float_rn(vals[e]);   // astype("<f4")
+    }
+    if (e < n_rew) reinterpret_cast<float *>(img + header + 12 * nnz)[e] = __double2float_rn(rewards[e]);
+}
+
+extern "C" int32_t fm_model_image(const uint64_t *d_block_off, int32_t n_blocks, const uint32_t *rows,
+                                  const uint32_t *cols, const double *vals, uint64_t nnz, const double *rewards,
+                                  uint64_t n_rewards, uint64_t header_bytes, unsigned char *d_img, void *stream)
+{
+    if (n_blocks < 1 || (header_bytes & 3)) return fm_fail(FM_BAD_ARG, "fm_model_image: bad layout");
+    const uint64_t n = nnz > n_rewards ? nnz : n_rewards;
+    if (n == 0) return FM_OK;
+    k_model_image<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        d_block_off, n_blocks, rows, cols, vals, nnz, rewards, n_rewards, header_bytes, d_img);
+    FM_CK_LAUNCH("k_model_image");
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Ensemble rollout (rollout.py:107-208): one thread per trajectory follows
+// the policy through its realization's flow, one step_flat per time index
+// (model_builder.py:286-369, want_cause) with the velocity of
+// reconstruct_at (environment.py:301-320).  Rows are recorded as (cell,
+// action, cause, reward, cumulative reward); the host formats them.
+// ---------------------------------------------------------------------------
+enum : int { C_MOVE = 0, C_TARGET = 1, C_OUTSIDE = 2, C_HORIZON = 3, C_LAND = 4, C_TRANSIT = 5 };
+
+struct RollK {
+    BuildK B;
+    const uint16_t *policy;
+    int si, sj;
+    const int32_t *real;
+    int n_traj, max_rows;
+    int32_t *row_cell;
+    int16_t *row_action;
+    int8_t *row_cause;
+    double *row_reward, *row_cum;
+    int32_t *n_rows, *final_cell;
+};
+
+__global__ void __launch_bounds__(128) k_rollout(const __grid_constant__ RollK R)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= R.n_traj) return;
+    const BuildK &K = R.B;
+    const int r = R.real[k];
+    const int rx = K.gate_r ? K.gate_r[0] : K.rx, ry = K.gate_r ? K.gate_r[1] : K.ry;
+    int cell = R.sj * K.nx + R.si;
+    double cum = 0.0;
+    int n = 0, fin = -1;
+    const size_t o = (size_t)k * R.max_rows;
+    for (int t = 0; t < K.nt; ++t) {
+        const int a = R.policy[(size_t)t * K.nc + cell];
+        const int ci = cell % K.nx, cj = cell / K.nx;
+        const fm_action A = K.act[a];
+        int cause, succ = 0;
+        double rw;
+        bool terminal;
+        if (t + 1 >= K.nt) {   // horizon (model_builder.py:319-328)
+            cause = C_HORIZON;
+            rw = K.r_out;
+            terminal = true;
+        } else {
+            double vx = K.mean[((size_t)t * K.nc + cell) * 2], vy = K.mean[((size_t)t * K.nc + cell) * 2 + 1];
+            for (int m = 0; m < K.nm; ++m) {
+                const double c = K.coeffs[((size_t)t * K.nr + r) * K.nm + m];
+                const double *md = K.modes + (((size_t)m * K.nt + t) * K.nc + cell) * 2;
+                vx = DADD(vx, DMUL(c, md[0]));
+                vy = DADD(vy, DMUL(c, md[1]));
+            }
+            const double x0 = DADD(K.ox, DMUL(DADD((double)ci, 0.5), K.dx));   // environment.py:96-103
+            const double y0 = DADD(K.oy, DMUL(DADD((double)cj, 0.5), K.dx));
+            const double x1 = DADD(x0, DMUL(DADD(vx, A.ax), K.dt)), y1 = DADD(y0, DMUL(DADD(vy, A.ay), K.dt));
+            const int i1 = __double2int_rd(to_cell<0>(x1, K.ox, K.dx, K.inv_dx));
+            const int j1 = __double2int_rd(to_cell<0>(y1, K.oy, K.dx, K.inv_dx));
+            const bool inb = (unsigned)i1 < (unsigned)K.nx && (unsigned)j1 < (unsigned)K.ny;
+            succ = inb ? j1 * K.nx + i1 : 0;
+            const bool landed = inb && K.mask[(size_t)(t + 1) * K.nc + succ] != 0;
+            bool blocked = false;
+            if (box_count(K, t, ci - rx, ci + rx, cj - ry, cj + ry) > 0) blocked = seg_blocked<0>(K, t, x0, y0, x1, y1);
+            const bool bad = !inb || landed || blocked;
+            const bool hit = inb && !bad && succ == K.tcell;
+            if (K.obj == FM_OBJ_NET_ENERGY) {
+                const double gs = K.g[(size_t)t * K.nc + cell];
+                const double gd = inb ? K.g[(size_t)(t + 1) * K.nc + succ] : 0.0;
+                const double b = DMUL(DADD(DADD(A.neg_cff, DMUL(K.h_cr, gs)), DMUL(K.h_cr, gd)), K.dt);
+                rw = hit ? DADD(b, K.r_term) : b;
+            } else {
+                rw = hit ? A.base_hit : A.base;
+            }
+            if (bad) rw = K.r_out;
+            cause = hit ? C_TARGET : C_MOVE;   // precedence of model_builder.py:363-366
+            if (blocked) cause = C_TRANSIT;
+            if (landed) cause = C_LAND;
+            if (!inb) cause = C_OUTSIDE;
+            terminal = bad;
+        }
+        cum = DADD(cum, rw);   // cum += reward (rollout.py:148)
+        R.row_cell[o + n] = cell;
+        R.row_action[o + n] = (int16_t)a;
+        R.row_cause[o + n] = (int8_t)cause;
+        R.row_reward[o + n] = rw;
+        R.row_cum[o + n] = cum;
+        ++n;
+        if (cause == C_TARGET) {
+            fin = succ;
+            break;
+        }
+        if (terminal) break;
+        cell = succ;
+    }
+    R.n_rows[k] = n;
+    R.final_cell[k] = fin;
+}
+
+extern "C" int32_t fm_rollout(const fm_rollout_args *h, void *stream)
+{
+    const fm_grid &G = h->grid;
+    if (G.nx < 1 || G.ny < 1 || G.nt < 1 || h->n_actions < 1 || h->n_traj < 0 || h->max_rows < G.nt)
+        return fm_fail(FM_BAD_ARG, "fm_rollout: bad arguments");
+    if (h->start_i < 0 || h->start_i >= G.nx || h->start_j < 0 || h->start_j >= G.ny)
+        return fm_fail(FM_BAD_ARG, "start cell (%d, %d) outside grid", h->start_i, h->start_j);
+    if (h->n_traj == 0) return FM_OK;
+    RollK R{};
+    BuildK &K = R.B;
+    K.nx = G.nx; K.ny = G.ny; K.nt = G.nt; K.nc = G.nx * G.ny;
+    K.dx = G.dx; K.dt = G.dt; K.ox = G.ox; K.oy = G.oy;
+    K.inv_dx = 1.0 / G.dx;
+    K.half_dx = 0.5 * G.dx;
+    K.mean = h->env.mean; K.modes = h->env.modes; K.coeffs = h->env.coeffs; K.g = h->env.g;
+    K.mask = h->env.mask; K.sat = h->mask_sat;
+    K.nm = h->env.n_modes; K.nr = h->env.n_real;
+    K.act = h->actions; K.na = h->n_actions; K.obj = h->reward.objective;
+    K.h_cr = 0.5 * h->reward.c_r;
+    K.r_term = h->reward.r_term; K.r_out = h->reward.r_outbound;
+    K.tcell = h->reward.target_j * G.nx + h->reward.target_i;
+    K.gate_r = h->d_gate_r;
+    R.policy = h->policy; R.si = h->start_i; R.sj = h->start_j;
+    R.real = h->realizations; R.n_traj = h->n_traj; R.max_rows = h->max_rows;
+    R.row_cell = h->row_cell; R.row_action = h->row_action; R.row_cause = h->row_cause;
+    R.row_reward = h->row_reward; R.row_cum = h->row_cum; R.n_rows = h->n_rows; R.final_cell = h->final_cell;
+    k_rollout<<<(h->n_traj + 127) / 128, 128, 0, (cudaStream_t)stream>>>(R);
+    FM_CK_LAUNCH("k_rollout");
+    return FM_OK;
+}

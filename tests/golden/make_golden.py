@@ -25,7 +25,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
-from golden_util import GOLDEN_JSON, env_digest, model_digest, sha  # noqa: E402
+from golden_util import GOLDEN_JSON, env_digest, model_digest, rows_digest, sha  # noqa: E402
 
 REF = "/root/reference/pkg"
 RANDOM_SEEDS = list(range(7000, 7020)) + [101, 301, 302, 303, 310, 320, 330] + list(range(401, 417)) + \
@@ -156,10 +156,79 @@ def main():
             out["named"][f"{name}_{obj}"] = rec
             print(name, obj, rec["nnz"], rec["solve"]["iterations_run"], rec["v_start"])
 
+    out["pipeline"] = pipeline_records(fm)
+    out["rollout"] = rollout_records(fm, conf)
     os.makedirs(os.path.dirname(GOLDEN_JSON), exist_ok=True)
     with open(GOLDEN_JSON, "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
     print("wrote", GOLDEN_JSON)
+
+
+def pipeline_records(fm):
+    """The reference's own file pipeline (pipeline.py:54-168): generate-env
+    -> build -> solve -> rollout on pkg/configs smoke + desk x 3 objectives,
+    in a scratch directory.  Records the SHA-256 of the model, policy and
+    trajectory files and the rollout summary (paths dropped)."""
+    import hashlib
+    from flowmdp import pipeline
+    from flowmdp.config import env_config_from_dict, run_config_from_dict
+
+    def fsha(path):
+        return hashlib.sha256(open(path, "rb").read()).hexdigest()
+
+    recs = {}
+    cfg_dir = os.path.join(REF, "configs")
+    work = tempfile.mkdtemp(prefix="flowmdp_pipe_")
+    cases = [("smoke", "smoke_env.json", "smoke_run.json", ("time", "energy", "net_energy")),
+             ("desk", "desk_env.json", "desk_run_time.json", ("time", "energy", "net_energy"))]
+    for name, env_file, run_file, objectives in cases:
+        env_cfg = env_config_from_dict(json.load(open(os.path.join(cfg_dir, env_file))))
+        env_dir = os.path.join(work, f"{name}_env")
+        pipeline.run_generate_env(env_cfg, env_dir)
+        base = json.load(open(os.path.join(cfg_dir, run_file)))
+        for obj in objectives:
+            d = dict(base)
+            d.update(environment=env_dir, objective=obj, threads=os.cpu_count() or 1,
+                     model=os.path.join(work, f"{name}_{obj}.model"),
+                     policy=os.path.join(work, f"{name}_{obj}.policy"),
+                     trajectories=os.path.join(work, f"{name}_{obj}.csv"),
+                     summary=os.path.join(work, f"{name}_{obj}.summary.json"))
+            cfg = run_config_from_dict(d)
+            b = pipeline.run_build(cfg)
+            sv = pipeline.run_solve(cfg)
+            ro = pipeline.run_rollout(cfg)
+            summary = {k: v for k, v in ro.items() if not k.endswith("_out")}
+            recs[f"{name}_{obj}"] = {
+                "run": {k: d[k] for k in ("objective", "c_f", "c_r", "r_term", "r_outbound", "n_headings",
+                                          "n_speeds", "f_max", "start", "target", "epsilon")},
+                "nnz_total": b["nnz_total"], "subgrid": [b["subgrid_half_width_x"], b["subgrid_half_width_y"]],
+                "iterations_run": sv["iterations_run"], "residual": sv["residual"], "converged": sv["converged"],
+                "model_file_sha": fsha(d["model"]), "policy_file_sha": fsha(d["policy"]),
+                "trajectories_csv_sha": fsha(d["trajectories"]), "summary": summary,
+            }
+            print("pipeline", name, obj, b["nnz_total"], sv["iterations_run"], recs[f"{name}_{obj}"]["model_file_sha"])
+    shutil.rmtree(work, ignore_errors=True)
+    return recs
+
+
+def rollout_records(fm, conf):
+    """Reference ensemble_rollout on random worlds under the reference's VI
+    policy; start = the non-target cell farthest from the target."""
+    from flowmdp.model_builder import StepContext, build_model, compute_subgrid
+    from flowmdp.rollout import ensemble_rollout
+    from flowmdp.solver import value_iteration
+    recs = {}
+    for seed in RANDOM_SEEDS[:16]:
+        env, acts, rcfg, target = conf.make_random_env(seed)
+        ctx = StepContext(env, acts, rcfg, target)
+        model = build_model(ctx, compute_subgrid(env.field, acts, env.grid))
+        pv = value_iteration(model)
+        g = env.grid
+        start = max(((i, j) for j in range(g.ny) for i in range(g.nx) if (i, j) != tuple(target)),
+                    key=lambda c: (abs(c[0] - target[0]) + abs(c[1] - target[1]), -c[1], -c[0]))
+        ens = ensemble_rollout(ctx, pv.actions, start)
+        recs[str(seed)] = {"start": list(start), "rows_sha": rows_digest(ens), "summary": ens.summary()}
+    return recs
 
 
 def _built(fm, env, acts, rcfg, target):
@@ -169,4 +238,13 @@ def _built(fm, env, acts, rcfg, target):
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--pipeline-only":
+        fm_, conf_ = _import_reference()
+        gold = json.load(open(GOLDEN_JSON))
+        gold["pipeline"] = pipeline_records(fm_)
+        gold["rollout"] = rollout_records(fm_, conf_)
+        with open(GOLDEN_JSON, "w") as fh:
+            json.dump(gold, fh, indent=1, sort_keys=True)
+        print("updated", GOLDEN_JSON)
+    else:
+        main()

@@ -51,3 +51,15 @@ def model_digest(model) -> str:
 def load_golden() -> dict:
     with open(GOLDEN_JSON) as fh:
         return json.load(fh)
+
+
+def rows_digest(ensemble) -> str:
+    """Digest of every trajectory of a rollout ensemble: outcome fields and
+    each row's values as repr (what the CSV writer prints)."""
+    h = hashlib.sha256()
+    for tr in ensemble.trajectories:
+        h.update(f"{tr.realization}|{tr.status}|{tr.final_cause}|{tr.n_steps}|{tr.arrival_t}|{tr.cum_reward!r}\n"
+                 .encode())
+        for row in tr.rows:
+            h.update(("|".join(repr(x) for x in row) + "\n").encode())
+    return h.hexdigest()

@@ -53,6 +53,9 @@ int main(void) {
          sizeof(fm_reward), sizeof(fm_model), sizeof(fm_build_args), sizeof(fm_violation), sizeof(fm_csr));
   printf("%zu %zu %zu %zu\n", offsetof(fm_build_args, mask_sat), offsetof(fm_build_args, viol_flags),
          offsetof(fm_model, capacity), offsetof(fm_model, d_nnz));
+  printf("%zu %zu %zu %zu\n", sizeof(fm_rollout_args), offsetof(fm_rollout_args, policy),
+         offsetof(fm_rollout_args, n_traj), offsetof(fm_rollout_args, final_cell));
+  printf("%zu %zu\n", offsetof(fm_build_args, h_actions), offsetof(fm_build_args, vmax_y));
   return 0;
 }
 """
@@ -72,6 +75,10 @@ def test_ctypes_layout_matches_header():
     assert ours == sizes
     assert offs == [_lib.FmBuildArgs.mask_sat.offset, _lib.FmBuildArgs.viol_flags.offset,
                     _lib.FmModel.capacity.offset, _lib.FmModel.d_nnz.offset]
+    R = _lib.FmRolloutArgs
+    assert [int(x) for x in lines[2].split()] == [C.sizeof(R), R.policy.offset, R.n_traj.offset,
+                                                  R.final_cell.offset]
+    assert [int(x) for x in lines[3].split()] == [_lib.FmBuildArgs.h_actions.offset, _lib.FmBuildArgs.vmax_y.offset]
 
 
 _HYPOT_PROBE = r"""
