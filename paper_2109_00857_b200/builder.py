@@ -311,6 +311,35 @@ class DeviceModel:
                             self.reward.data_ptr(), self.entries.data_ptr(),
                             int(self.entries.numel()), self.d_nnz.data_ptr())
 
+    def rows_coo(self, t: int, a: int, j0: int, j1: int):
+        """Canonical COO of action a, layer t, source rows j in [j0, j1) (host
+        arrays rows u32, cols u32, vals f64, rewards f64 per cell) gathered
+        from the compact model -- for spot checks of models too large to
+        export whole."""
+        torch = _torch()
+        self.check()
+        g, na = self.grid, self.n_actions
+        nc = g.nx * g.ny
+        cells = torch.arange(j0 * g.nx, j1 * g.nx, device=self.row_ptr.device, dtype=torch.int64)
+        rid = (t * nc + cells) * na + a
+        ptr = self.row_ptr[rid]
+        cnt = self.row_nnz[rid].to(torch.int64) & 0xFFFF
+        idx = torch.repeat_interleave(ptr, cnt) + (torch.arange(int(cnt.sum()), device=ptr.device)
+                                                   - torch.repeat_interleave(torch.cumsum(cnt, 0) - cnt, cnt))
+        ent = self.entries[idx].to(torch.int64) & 0xFFFFFFFF
+        src = torch.repeat_interleave(cells, cnt)
+        slot, count = ent >> 16, ent & 0xFFFF
+        hx, hy = self.subgrid.half_width_x, self.subgrid.half_width_y
+        W = 2 * hx + 1
+        nslot = W * (2 * hy + 1)
+        di, dj = slot % W - hx, slot // W - hy
+        col = (t + 1) * nc + (src // g.nx + dj) * g.nx + (src % g.nx + di)
+        col = torch.where(slot == nslot, torch.full_like(col, g.nt * nc), col)
+        rows = (t * nc + src).cpu().numpy().astype(np.uint32)
+        # true division on the host (a device tensor / scalar may multiply by the reciprocal)
+        vals = count.cpu().numpy().astype(np.float64) / float(self.n_real)
+        return rows, col.cpu().numpy().astype(np.uint32), vals, self.reward[rid].cpu().numpy()
+
     def export_device(self):
         """Canonical COO on the device: (block_off, rows, cols, vals, rewards)."""
         torch = _torch()

@@ -330,3 +330,14 @@ def test_model_buffer_reuse():
     fresh = build_device_model(de, acts, rcfg, target, sub, j_range=(1, 3))
     import torch
     assert torch.equal(part.row_nnz, fresh.row_nnz) and torch.equal(part.reward, fresh.reward)
+
+
+@pytest.mark.parametrize("heads", [16, 12])
+def test_wide_action_sets_parity(heads):
+    """|A| = 32 and 24 (one source cell per warp, C5's action count) on the
+    desk world, time and net_energy, every block against the oracle."""
+    env, _, _, target, _ = make_named_env("desk")
+    acts = ActionSpace(n_headings=heads, n_speeds=2, f_max=1.0)
+    for obj in ("time", "net_energy"):
+        rcfg = RewardConfig(obj, c_f=1.0, c_r=0.5, r_term=100.0, r_outbound=-300.0)
+        _gpu_case(env, acts, rcfg, target)
