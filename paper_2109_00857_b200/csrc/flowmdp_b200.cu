@@ -435,6 +435,25 @@ struct BuildK {
     unsigned int *task_counter;
 };
 
+// fl(q / n) for 0 <= q <= n <= kFracMaxN at g_frac[n (n + 1) / 2 + q]: the
+// segment-sampling fractions of environment.py:361 without a division each
+static constexpr int kFracMaxN = 96;
+__device__ double g_frac[(kFracMaxN + 1) * (kFracMaxN + 2) / 2];
+
+static int32_t frac_table_init()
+{
+    static int dev_done = -1;
+    int dev = 0;
+    FM_CK(cudaGetDevice(&dev));
+    if (dev_done == dev) return FM_OK;
+    std::vector<double> h((kFracMaxN + 1) * (kFracMaxN + 2) / 2);
+    for (int n = 1; n <= kFracMaxN; ++n)
+        for (int q = 0; q <= n; ++q) h[n * (n + 1) / 2 + q] = (double)q / (double)n;   // IEEE, correctly rounded
+    FM_CK(cudaMemcpyToSymbol(g_frac, h.data(), h.size() * sizeof(double)));
+    dev_done = dev;
+    return FM_OK;
+}
+
 // count of set mask cells at layer t inside [i0,i1] x [j0,j1] (clipped)
 __device__ __forceinline__ int box_count(const BuildK &K, int t, int i0, int i1, int j0, int j1)
 {
@@ -479,8 +498,10 @@ __device__ __forceinline__ bool seg_blocked(const BuildK &K, int t, double p0x, 
     FM_STAT(1, 1);
     FM_STAT(2, n + 1);
     const uint8_t *mt = K.mask + (size_t)t * K.nc;
+    const double *ftab = n <= kFracMaxN ? g_frac + n * (n + 1) / 2 : nullptr;
     for (long long q = 0; q <= n; ++q) {
-        double frac = DDIV((double)q, ns);
+        // fl(q / n): tabulated correctly rounded quotients for small n
+        double frac = ftab ? ftab[q] : DDIV((double)q, ns);
         if (frac > 1.0) frac = 1.0;
         const double px = DADD(p0x, DMUL(frac, ddx));
         const double py = DADD(p0y, DMUL(frac, ddy));
@@ -653,9 +674,8 @@ __device__ __forceinline__ int floor_magic(double u)
 // overridden here; everything else goes to rare_transition.
 template <int FLAGS, bool EDGE, bool OBST>
 __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, const double2 v,
-                                                const double *__restrict__ g_n, const uint32_t *dang,
-                                                const uint32_t *dseg, const uint32_t *dloose, int outq, int &q,
-                                                double &rw)
+                                                const double *__restrict__ g_n, const uint32_t *cls, int outq,
+                                                int &q, double &rw)
 {
     double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
     if (!(FLAGS & F_DT_ONE)) {
@@ -688,29 +708,22 @@ __device__ __forceinline__ bool fast_transition(const BuildK &K, const RowC &R, 
     bool ok = inwin;
     if (OBST) {
         const int slot = q + R.soff;
-        const unsigned bit = 1u << (slot & 31);
-        // landing cell masked at t+1: bad whatever the transit (model_builder.py:336, 347)
-#ifdef FM_NO_LAND_INLINE
-        const bool land = false;
-        (void)dseg;
-        const bool segd = inwin && ((dang[slot >> 5] | dloose[slot >> 5]) & bit);
-#else
-        const bool land = inwin && (dang[slot >> 5] & bit);
-        // gated segment whose box touches the mask at t: exact test needed
-        // gated segment: its sample cells lie in the box spanned by the source
-        // cell and the cell of ex = x0 + (x1 - x0) (seg_blocked); `tight` =
-        // that box with ex's cell = the landing cell touches the mask at t,
-        // `loose` = the same box grown by one cell (covers any ex)
-        const bool tight = inwin && !land && (dseg[slot >> 5] & bit);
-        const bool loose = inwin && !land && (dloose[slot >> 5] & bit);
-        bool segd = tight;
-        if (loose && !tight) {   // blocked only if ex leaves the landing cell
+        // slot class (2 bits per slot, see the danger map in k_build):
+        // 1 landing cell masked at t+1 -> bad whatever the transit
+        //   (model_builder.py:336, 347), settled here;
+        // 2 gated segment whose tight box (source cell x landing cell)
+        //   touches the mask at t -> exact test;
+        // 3 only the box grown by one cell touches it -> exact test only if
+        //   the transit end ex = x0 + (x1 - x0) leaves the landing cell
+        const int c = inwin ? (int)((cls[slot >> 4] >> ((slot & 15) << 1)) & 3u) : 0;
+        const bool land = c == 1;
+        bool segd = c == 2;
+        if (c == 3) {
             const double ex = DADD(R.x0, DSUB(x1, R.x0)), ey = DADD(R.y0, DSUB(y1, R.y0));
             const int ei = __double2int_rd(to_cell<FLAGS>(ex, K.ox, K.dx, K.inv_dx));
             const int ej = __double2int_rd(to_cell<FLAGS>(ey, K.oy, K.dx, K.inv_dx));
             segd = ei != i1 || ej != j1;
         }
-#endif
         const bool dead = R.rflags & RF_DEAD;
         ok = inwin && (!segd || dead);
         if (land) {
@@ -874,6 +887,68 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
     }
 }
 
+// Landing slot of one transition in an obstacle warp under F_PROVEN | F_CNT
+// (rewards come from the counts, so only the slot is needed).  Landings
+// outside the domain stay in their (unclipped) window slot -- class 0 --
+// and are folded into OUT in the epilogue; `rare` = exact segment test.
+template <int FLAGS>
+__device__ __forceinline__ int obst_slot(const BuildK &K, const RowC &R, const double2 v, const uint32_t *cls,
+                                         int outq, bool &rare)
+{
+    double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
+    if (!(FLAGS & F_DT_ONE)) {
+        px = DMUL(px, K.dt);
+        py = DMUL(py, K.dt);
+    }
+    const double x1 = DADD(R.x0, px), y1 = DADD(R.y0, py);
+    const int i1 = floor_magic(to_cell<FLAGS>(x1, K.ox, K.dx, K.inv_dx));
+    const int j1 = floor_magic(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx));
+    const int q = j1 * K.width + i1, slot = q + R.soff;
+    const int c = (int)((cls[slot >> 4] >> ((slot & 15) << 1)) & 3u);   // see fast_transition
+    rare = c == 2;
+    if (c == 3) {
+        const double ex = DADD(R.x0, DSUB(x1, R.x0)), ey = DADD(R.y0, DSUB(y1, R.y0));
+        rare = floor_magic(to_cell<FLAGS>(ex, K.ox, K.dx, K.inv_dx)) != i1 ||
+               floor_magic(to_cell<FLAGS>(ey, K.oy, K.dx, K.inv_dx)) != j1;
+    }
+    return c == 1 ? outq : q;
+}
+
+// Obstacle-warp realization loop under F_PROVEN | F_CNT for the live (not
+// dead) rows: 4 transitions per step, one vote sends exact segment tests to
+// the rare path, shared-memory reductions into the histogram.
+template <int FLAGS>
+__device__ __forceinline__ void chunk_rows_obst_cnt(const BuildK *__restrict__ Kg, int t, const RowC &R,
+                                                    const double2 *vrow, int nk, const uint32_t *cls,
+                                                    uint16_t *h16q, int outq, unsigned livemask, unsigned half_one)
+{
+    const BuildK &K = *Kg;
+    const unsigned hs_word = (unsigned)__cvta_generic_to_shared(h16q) & ~3u;
+    int k = 0;
+    for (; k + 4 <= nk; k += 4) {
+        double2 v[4];
+        int q[4];
+        bool r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = vrow[k + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = obst_slot<FLAGS>(K, R, v[u], cls, outq, r[u]);
+        if (!__all_sync(livemask, !(r[0] || r[1] || r[2] || r[3]))) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (r[u]) q[u] = rare_transition<FLAGS>(Kg, t, R, v[u]).slot;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) hist_inc(h16q, hs_word, q[u], half_one);
+    }
+    for (; k < nk; ++k) {
+        bool r0;
+        int q0 = obst_slot<FLAGS>(K, R, vrow[k], cls, outq, r0);
+        if (r0) q0 = rare_transition<FLAGS>(Kg, t, R, vrow[k]).slot;
+        hist_inc(h16q, hs_word, q0, half_one);
+    }
+}
+
 // The realization loop of one chunk for the row lanes: 4 independent
 // transitions per iteration in straight-line code (interleaved by the
 // compiler), one warp vote to divert rare lanes, reward sums in ascending r.
@@ -881,8 +956,7 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
 template <int FLAGS, bool EDGE, bool OBST>
 __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__restrict__ Kg, int t, const RowC &R,
                                            const double2 *vrow, int nk, const double *__restrict__ g_n,
-                                           const uint32_t *dang, const uint32_t *dseg, const uint32_t *dloose,
-                                           uint16_t *h16q, int outq,
+                                           const uint32_t *cls, uint16_t *h16q, int outq,
                                            unsigned rowmask, double &S, int &viol)
 {
     int k = 0;
@@ -890,10 +964,10 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
         const double2 v0 = vrow[k], v1 = vrow[k + 1], v2 = vrow[k + 2], v3 = vrow[k + 3];
         int q0, q1, q2, q3;
         double w0, w1, w2, w3;
-        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, v0, g_n, dang, dseg, dloose, outq, q0, w0);
-        const bool f1 = fast_transition<FLAGS, EDGE, OBST>(K, R, v1, g_n, dang, dseg, dloose, outq, q1, w1);
-        const bool f2 = fast_transition<FLAGS, EDGE, OBST>(K, R, v2, g_n, dang, dseg, dloose, outq, q2, w2);
-        const bool f3 = fast_transition<FLAGS, EDGE, OBST>(K, R, v3, g_n, dang, dseg, dloose, outq, q3, w3);
+        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, v0, g_n, cls, outq, q0, w0);
+        const bool f1 = fast_transition<FLAGS, EDGE, OBST>(K, R, v1, g_n, cls, outq, q1, w1);
+        const bool f2 = fast_transition<FLAGS, EDGE, OBST>(K, R, v2, g_n, cls, outq, q2, w2);
+        const bool f3 = fast_transition<FLAGS, EDGE, OBST>(K, R, v3, g_n, cls, outq, q3, w3);
         if (!__all_sync(rowmask, f0 && f1 && f2 && f3)) {
             if (!f0) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v0); q0 = o.slot; w0 = o.rw; viol |= o.viol; }
             if (!f1) { const SlowOut o = rare_transition<FLAGS>(Kg, t, R, v1); q1 = o.slot; w1 = o.rw; viol |= o.viol; }
@@ -912,7 +986,7 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
     for (; k < nk; ++k) {
         int q0;
         double w0;
-        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, vrow[k], g_n, dang, dseg, dloose, outq, q0, w0);
+        const bool f0 = fast_transition<FLAGS, EDGE, OBST>(K, R, vrow[k], g_n, cls, outq, q0, w0);
         if (!f0) {
             const SlowOut o = rare_transition<FLAGS>(Kg, t, R, vrow[k]);
             q0 = o.slot;
@@ -1065,45 +1139,53 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
         } else {
             const bool edge = __any_sync(kFull, edge_row);
             const unsigned rowmask = __ballot_sync(kFull, row_ok);   // lanes that run chunk_rows
+            const unsigned livemask = __ballot_sync(kFull, row_ok && !(R.rflags & RF_DEAD));
             const bool obst = PART == 1   ? false
                               : PART == 2 ? true
                                           : __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
-            const int DW = (nslot + 31) >> 5;
+            const int DW = (nslot + 31) >> 5, CWD = 2 * DW;   // class words per cell
             if (obst) {
-                // danger[0][cs][slot]: landing cell masked at t+1 (bad, settled
-                // inline); danger[1][cs][slot]: (gated cell) the segment box
-                // [min(c,l)-1, max(c,l)+1] touches the mask at t (exact test)
+                // danger map: 2-bit class per (cell, window slot), 16 slots per
+                // word: 0 safe, 1 landing cell masked at t+1, 2 gated with the
+                // tight box [min(c,l), max(c,l)] touching the mask at t, 3
+                // gated with only the box grown by one cell touching it
                 for (int wd = 0; wd < CW * DW; ++wd) {
                     const int cs = wd / DW, sl = (wd - cs * DW) * 32 + lane;
                     const int lc = grp * CW + cs;
-                    bool land = false, tight = false, loose = false;
+                    unsigned c = 0;
                     if (lc < K.ncell && sl < nslot) {
                         const int cc = K.cell0 + lc, cci = cc % K.nx, ccj = cc / K.nx;
                         const int li = cci + sl % W - K.hx, lj = ccj + sl / W - K.hy;
                         if ((unsigned)li < (unsigned)K.nx && (unsigned)lj < (unsigned)K.ny) {
-                            land = K.mask[(size_t)(t + 1) * K.nc + lj * K.nx + li] != 0;
-                            if (!land && box_count(K, t, cci - rx, cci + rx, ccj - ry, ccj + ry) > 0) {
-                                loose = box_count(K, t, min(cci, li) - 1, max(cci, li) + 1, min(ccj, lj) - 1,
-                                                  max(ccj, lj) + 1) > 0;
+                            if (K.mask[(size_t)(t + 1) * K.nc + lj * K.nx + li]) {
+                                c = 1;
+                            } else if (box_count(K, t, cci - rx, cci + rx, ccj - ry, ccj + ry) > 0 &&
+                                       box_count(K, t, min(cci, li) - 1, max(cci, li) + 1, min(ccj, lj) - 1,
+                                                 max(ccj, lj) + 1) > 0) {
                                 // tight needs cell(x0) == source cell (host-checked)
-                                tight = loose && (!K.src_cell_exact ||
-                                                  box_count(K, t, min(cci, li), max(cci, li), min(ccj, lj),
-                                                            max(ccj, lj)) > 0);
+                                c = (!K.src_cell_exact || box_count(K, t, min(cci, li), max(cci, li),
+                                                                    min(ccj, lj), max(ccj, lj)) > 0) ? 2 : 3;
                             }
                         }
                     }
-                    const unsigned wl = __ballot_sync(kFull, land), wt = __ballot_sync(kFull, tight),
-                                   wo = __ballot_sync(kFull, loose);
-                    if (lane == 0) {
-                        danger[wd] = wl;
-                        danger[CW * DW + wd] = wt;
-                        danger[2 * CW * DW + wd] = wo;
+                    // pack: lane l's class -> bits 2(l & 15) of word (l >> 4)
+                    const unsigned w0 = __ballot_sync(kFull, c & 1u), w1 = __ballot_sync(kFull, c & 2u);
+                    if (lane < 2) {
+                        unsigned lo = (w0 >> (16 * lane)) & 0xFFFFu, hi = (w1 >> (16 * lane)) & 0xFFFFu;
+                        lo = (lo | (lo << 8)) & 0x00FF00FFu;   // spread 16 bits to even positions
+                        lo = (lo | (lo << 4)) & 0x0F0F0F0Fu;
+                        lo = (lo | (lo << 2)) & 0x33333333u;
+                        lo = (lo | (lo << 1)) & 0x55555555u;
+                        hi = (hi | (hi << 8)) & 0x00FF00FFu;
+                        hi = (hi | (hi << 4)) & 0x0F0F0F0Fu;
+                        hi = (hi | (hi << 2)) & 0x33333333u;
+                        hi = (hi | (hi << 1)) & 0x55555555u;
+                        danger[cs * CWD + (wd - cs * DW) * 2 + lane] = lo | (hi << 1);
                     }
                 }
                 __syncwarp();
             }
-            const uint32_t *dang = danger + cs_row * DW, *dseg = danger + (CW + cs_row) * DW,
-                           *dloose = danger + (2 * CW + cs_row) * DW;
+            const uint32_t *cls = danger + cs_row * CWD;
             // fast-path form of the row constants: target slot and OUT slot in
             // q = slot - soff coordinates, histogram pointer shifted by soff
             RowC Rf = R;
@@ -1212,12 +1294,17 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                 const int nk = min(RC, nr - r0);
                 if (row_ok) {
                     FM_STAT(obst ? 3 : 4, nk);
-                    if (obst) {
+                    if ((FLAGS & F_PROVEN) && (FLAGS & F_CNT) && obst) {
+                        // dead rows count nothing: no overflow test is needed
+                        // under F_PROVEN and their counts are all OUT
+                        if (!(R.rflags & RF_DEAD))
+                            chunk_rows_obst_cnt<FLAGS>(Kg, t, Rf, vrow, nk, cls, h16q, outq, livemask, half_one);
+                    } else if (obst) {
                         if (edge)
-                            chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, dloose, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, cls, h16q, outq, rowmask, S,
                                                           viol);
                         else
-                            chunk_rows<FLAGS, false, true>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, dloose, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, false, true>(K, Kg, t, Rf, vrow, nk, g_n, cls, h16q, outq, rowmask, S,
                                                            viol);
                     } else if (FLAGS & F_PROVEN) {
                         // F_CNT: edge rows count out-of-domain landings in their
@@ -1232,20 +1319,18 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                             chunk_rows_lean<FLAGS, false>(K, Rf, vrow, nk, g_n, h16q, outq, S, half_one);
                     } else {
                         if (edge)
-                            chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, dloose, h16q, outq, rowmask, S,
+                            chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, cls, h16q, outq, rowmask, S,
                                                            viol);
                         else
-                            chunk_rows<FLAGS, false, false>(K, Kg, t, Rf, vrow, nk, g_n, dang, dseg, dloose, h16q, outq, rowmask,
+                            chunk_rows<FLAGS, false, false>(K, Kg, t, Rf, vrow, nk, g_n, cls, h16q, outq, rowmask,
                                                             S, viol);
                     }
                 }
                 __syncwarp();
             }
-#ifdef FM_NO_EDGE_FOLD
-            if (false) {
-#else
-            if ((FLAGS & F_CNT) && !obst && row_ok && edge_row) {
-#endif
+            const bool dead_row = row_ok && (R.rflags & RF_DEAD);
+            if ((FLAGS & F_CNT) && dead_row) h16[nslot * 32] = (uint16_t)nr;   // every realization -> SINK
+            if ((FLAGS & F_CNT) && row_ok && edge_row && !dead_row) {
                 // window slots whose cell lies outside the domain held the
                 // landings that leave it: SINK (model_builder.py:331-335, 347)
                 int extra = 0;
@@ -1261,16 +1346,18 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                 }
                 h16[nslot * 32] += (uint16_t)extra;
             }
-            if ((FLAGS & F_CNT) && !obst && row_ok) {
+            if ((FLAGS & F_CNT) && row_ok) {
                 // exact reward sum from the counts (F_CNT): every partial sum
                 // of the reference's sequential loop is exactly representable,
-                // so it equals n_norm*base + n_hit*base_hit + n_out*r_out;
+                // so it equals n_norm*base + n_hit*base_hit + n_out*r_out
+                // (dead rows: all OUT; the target's rewards are 0.0);
                 // + 0.0 turns a -0.0 into the loop's +0.0
                 const int n_out = h16[nslot * 32], n_hit = R.tslot >= 0 ? h16[R.tslot * 32] : 0;
                 const int n_norm = nr - n_out - n_hit;
                 S = DADD(DADD(DADD(DMUL((double)n_norm, R.base), DMUL((double)n_hit, R.base_hit)),
                               DMUL((double)n_out, K.r_out)),
                          0.0);
+                if (R.rflags & RF_TERMINAL) S = 0.0;
             }
         }
 
@@ -1542,7 +1629,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.off_coef = K.off_vbuf + K.CW * (K.RC + 1) * (int)sizeof(double2);
     K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
     K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
-    K.smem_warp = align16(K.off_danger + 3 * K.CW * (int)((nslot + 31) / 32) * 4);
+    K.smem_warp = align16(K.off_danger + 2 * K.CW * (int)((nslot + 31) / 32) * 4);
     K.src_cell_exact = source_cells_exact(G) ? 1 : 0;
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
     K.entries = M->entries; K.capacity = M->capacity;
@@ -1570,6 +1657,8 @@ extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *st
     BuildK K;
     int flags = 0;
     int32_t st = build_params(h, M, K, flags);
+    if (st != FM_OK) return st;
+    st = frac_table_init();
     if (st != FM_OK) return st;
     FM_CK(cudaMemsetAsync(h->task_counter, 0, sizeof(unsigned int), s));
     return launch_build(K, flags, (size_t)4 * K.smem_warp, s);
