@@ -424,6 +424,7 @@ struct BuildK {
     long long n_tasks;
     // per-warp shared-memory carve-up (bytes)
     int smem_warp, off_vbuf, off_coef, off_modes, off_danger;
+    int off_queue;   // PART 2 (F_PROVEN | F_CNT): deferred exact-test queue [kQueue]
     // outputs
     uint64_t *row_ptr;
     uint16_t *row_nnz;
@@ -508,6 +509,33 @@ __device__ __forceinline__ bool seg_blocked(const BuildK &K, int t, double p0x, 
         const long long i = __double2ll_rd(to_cell<FLAGS>(px, K.ox, K.dx, K.inv_dx));
         const long long j = __double2ll_rd(to_cell<FLAGS>(py, K.oy, K.dx, K.inv_dx));
         if (i >= 0 && i < K.nx && j >= 0 && j < K.ny && mt[j * K.nx + i]) return true;
+    }
+    return false;
+}
+
+// The sampling part of _segments_blocked (environment.py:353-367) without
+// the box prefilter, for segments already known to need it.
+template <int FLAGS>
+__device__ __forceinline__ bool seg_samples_blocked(const BuildK &K, int t, double p0x, double p0y, double p1x,
+                                                    double p1y)
+{
+    const double ddx = DSUB(p1x, p0x), ddy = DSUB(p1y, p0y);
+    const double len = fm_hypot(ddx, ddy);
+    double ns = ceil(DDIV(len, K.half_dx));
+    if (!(ns >= 1.0)) ns = 1.0;
+    const long long n = (long long)ns;
+    FM_STAT(1, 1);
+    FM_STAT(2, n + 1);
+    const uint8_t *mt = K.mask + (size_t)t * K.nc;
+    const double *ftab = n <= kFracMaxN ? g_frac + n * (n + 1) / 2 : nullptr;
+    for (long long q = 0; q <= n; ++q) {
+        double frac = ftab ? ftab[q] : DDIV((double)q, ns);
+        if (frac > 1.0) frac = 1.0;
+        const double px = DADD(p0x, DMUL(frac, ddx));
+        const double py = DADD(p0y, DMUL(frac, ddy));
+        const long long i = __double2ll_rd(to_cell<FLAGS>(px, K.ox, K.dx, K.inv_dx));
+        const long long j = __double2ll_rd(to_cell<FLAGS>(py, K.oy, K.dx, K.inv_dx));
+        if (i >= 0 && i < K.nx && j >= 0 && j < K.ny && __ldg(mt + j * K.nx + i)) return true;
     }
     return false;
 }
@@ -914,17 +942,29 @@ __device__ __forceinline__ int obst_slot(const BuildK &K, const RowC &R, const d
     return c == 1 ? outq : q;
 }
 
+// A deferred exact segment test: transit end, owner lane, landing slot.
+struct QItem {
+    double x1, y1;
+    int32_t meta;   // owner lane << 16 | landing slot (window index, < 65535)
+};
+static constexpr int kQueue = 64;
+
 // Obstacle-warp realization loop under F_PROVEN | F_CNT for the live (not
-// dead) rows: 4 transitions per step, one vote sends exact segment tests to
-// the rare path, shared-memory reductions into the histogram.
+// dead) rows.  Counts commute (rewards come from the counts), so exact
+// segment tests are deferred to the end of the chunk and run by all lanes
+// that have one at once -- one pass per pending item of the busiest lane --
+// instead of one divergent call per batch position (the deferred items are
+// marked in a 64-bit mask of chunk-local realizations).
 template <int FLAGS>
 __device__ __forceinline__ void chunk_rows_obst_cnt(const BuildK *__restrict__ Kg, int t, const RowC &R,
                                                     const double2 *vrow, int nk, const uint32_t *cls,
-                                                    uint16_t *h16q, int outq, unsigned livemask, unsigned half_one)
+                                                    uint16_t *h16q, int outq, bool live, unsigned half_one,
+                                                    unsigned char *qbase, unsigned hist_s, int grp)
 {
     const BuildK &K = *Kg;
     const unsigned hs_word = (unsigned)__cvta_generic_to_shared(h16q) & ~3u;
-    int k = 0;
+    unsigned long long pend = 0;
+    int k = live ? 0 : nk;
     for (; k + 4 <= nk; k += 4) {
         double2 v[4];
         int q[4];
@@ -933,20 +973,75 @@ __device__ __forceinline__ void chunk_rows_obst_cnt(const BuildK *__restrict__ K
         for (int u = 0; u < 4; ++u) v[u] = vrow[k + u];
 #pragma unroll
         for (int u = 0; u < 4; ++u) q[u] = obst_slot<FLAGS>(K, R, v[u], cls, outq, r[u]);
-        if (!__all_sync(livemask, !(r[0] || r[1] || r[2] || r[3]))) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (r[u]) q[u] = rare_transition<FLAGS>(Kg, t, R, v[u]).slot;
+        for (int u = 0; u < 4; ++u) {
+            if (r[u]) pend |= 1ull << ((k + u) & 63);
+            else hist_inc(h16q, hs_word, q[u], half_one);
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) hist_inc(h16q, hs_word, q[u], half_one);
     }
     for (; k < nk; ++k) {
         bool r0;
-        int q0 = obst_slot<FLAGS>(K, R, vrow[k], cls, outq, r0);
-        if (r0) q0 = rare_transition<FLAGS>(Kg, t, R, vrow[k]).slot;
-        hist_inc(h16q, hs_word, q0, half_one);
+        const int q0 = obst_slot<FLAGS>(K, R, vrow[k], cls, outq, r0);
+        if (r0) pend |= 1ull << (k & 63);
+        else hist_inc(h16q, hs_word, q0, half_one);
     }
+#ifndef FM_EXPERIMENT_NO_RARE   // timing experiment only: wrong results
+    // drain: the live lanes park their deferred transitions in the warp's
+    // queue, then every lane of the warp takes queue entries round-robin
+    // (the exact tests of one busy row are spread over all 32 lanes)
+    QItem *queue = reinterpret_cast<QItem *>(qbase);
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        const int mine = __popcll(pend);
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(kFull, incl, 31);
+        if (total == 0) break;
+        int pos = incl - mine;
+        while (pend && pos < kQueue) {
+            const int kk = __ffsll((long long)pend) - 1;
+            pend &= pend - 1;
+            const double2 v = vrow[kk];
+            double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);
+            if (!(FLAGS & F_DT_ONE)) {
+                px = DMUL(px, K.dt);
+                py = DMUL(py, K.dt);
+            }
+            const double x1 = DADD(R.x0, px), y1 = DADD(R.y0, py);
+            const int q = floor_magic(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx)) * K.width +
+                          floor_magic(to_cell<FLAGS>(x1, K.ox, K.dx, K.inv_dx));
+            queue[pos].x1 = x1;
+            queue[pos].y1 = y1;
+            queue[pos].meta = (lane << 16) | (q + R.soff);
+            ++pos;
+        }
+        __syncwarp();
+        const int n_q = total < kQueue ? total : kQueue;
+        for (int e = lane; e < n_q; e += 32) {
+            // the deferred transition lands in-domain on an unmasked cell
+            // (class 2/3): only the transit samples decide (env.py:353-367)
+            const QItem it = queue[e];
+            const int owner = it.meta >> 16, slot = it.meta & 0xFFFF;
+            const int c = K.cell0 + grp * K.CW + owner / K.AG;
+            const double x0 = DADD(K.ox, DMUL(DADD((double)(c % K.nx), 0.5), K.dx));   // environment.py:99-100
+            const double y0 = DADD(K.oy, DMUL(DADD((double)(c / K.nx), 0.5), K.dx));
+#ifdef FM_EXPERIMENT_NO_SEG   // timing experiment only: wrong results
+            const int sl = (x0 == it.x1 && y0 == it.y1) ? K.nslot : slot;
+#else
+            const int sl = seg_samples_blocked<FLAGS>(K, t, x0, y0, it.x1, it.y1) ? K.nslot : slot;
+#endif
+            // the owner's u16 counter [slot][owner] lives in word (slot * 16 + owner / 2)
+            asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(hist_s + (unsigned)sl * 64u + (unsigned)(owner >> 1) * 4u),
+                         "r"(1u << ((owner & 1) * 16))
+                         : "memory");
+        }
+        __syncwarp();
+    }
+#endif
 }
 
 // The realization loop of one chunk for the row lanes: 4 independent
@@ -1023,6 +1118,7 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
 #ifndef FM_BUILD_RC
 #define FM_BUILD_RC 64
 #endif
+static_assert(FM_BUILD_RC <= 64, "chunk_rows_obst_cnt marks deferred realizations in a 64-bit mask");
 template <int FLAGS, int PART>
 __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_constant__ BuildK K)
 {
@@ -1139,7 +1235,6 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
         } else {
             const bool edge = __any_sync(kFull, edge_row);
             const unsigned rowmask = __ballot_sync(kFull, row_ok);   // lanes that run chunk_rows
-            const unsigned livemask = __ballot_sync(kFull, row_ok && !(R.rflags & RF_DEAD));
             const bool obst = PART == 1   ? false
                               : PART == 2 ? true
                                           : __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
@@ -1292,14 +1387,16 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                 __syncwarp();
                 if (r0 + RC < nr) issue_chunk(r0 + RC);   // lands while the rows work
                 const int nk = min(RC, nr - r0);
-                if (row_ok) {
+                if ((FLAGS & F_PROVEN) && (FLAGS & F_CNT) && obst) {
+                    // whole warp (the drain is warp-cooperative); dead rows
+                    // count nothing: no overflow test is needed under
+                    // F_PROVEN and their counts are all OUT
+                    chunk_rows_obst_cnt<FLAGS>(Kg, t, Rf, vrow, nk, cls, h16q, outq,
+                                               row_ok && !(R.rflags & RF_DEAD), half_one, wbase + K.off_queue,
+                                               (unsigned)__cvta_generic_to_shared(hist16), grp);
+                } else if (row_ok) {
                     FM_STAT(obst ? 3 : 4, nk);
-                    if ((FLAGS & F_PROVEN) && (FLAGS & F_CNT) && obst) {
-                        // dead rows count nothing: no overflow test is needed
-                        // under F_PROVEN and their counts are all OUT
-                        if (!(R.rflags & RF_DEAD))
-                            chunk_rows_obst_cnt<FLAGS>(Kg, t, Rf, vrow, nk, cls, h16q, outq, livemask, half_one);
-                    } else if (obst) {
+                    if (obst) {
                         if (edge)
                             chunk_rows<FLAGS, true, true>(K, Kg, t, Rf, vrow, nk, g_n, cls, h16q, outq, rowmask, S,
                                                           viol);
@@ -1436,6 +1533,8 @@ __global__ void k_viol_report(const __grid_constant__ BuildK K, int t, int a, in
     }
 }
 
+static int align16(int x) { return (x + 15) & ~15; }
+
 template <int FL, int PART>
 static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
 {
@@ -1458,7 +1557,15 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
     } else {
         const int32_t st = launch_build_p<FL, 1>(K, smem, s);
         if (st != FM_OK) return st;
-        return launch_build_p<FL, 2>(K, smem, s);
+        if constexpr ((FL & F_CNT) != 0) {
+            // obstacle part: per-warp queue of deferred exact segment tests
+            BuildK K2 = K;
+            K2.off_queue = K.smem_warp;
+            K2.smem_warp = align16(K.smem_warp + kQueue * (int)sizeof(QItem));
+            return launch_build_p<FL, 2>(K2, (size_t)4 * K2.smem_warp, s);
+        } else {
+            return launch_build_p<FL, 2>(K, smem, s);
+        }
     }
 }
 
@@ -1497,7 +1604,6 @@ static bool is_pow2(double x)
     return m == 0.5;
 }
 
-static int align16(int x) { return (x + 15) & ~15; }
 
 // One axis of the lean-path proof.  reach = fl(fl(vmax + amax) * dt) bounds
 // |fl(fl(v + a) * dt)| for every transition (|v| <= vmax exactly: it is the
