@@ -854,7 +854,14 @@ __device__ __forceinline__ void hist_inc(uint16_t *h16q, unsigned hs_word, int q
 {
 #ifdef FM_HIST_ATOMS
     (void)h16q;
+#ifdef FM_RED_CLOBBER
     asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(hs_word + (unsigned)q * 64u), "r"(half_one) : "memory");
+#else
+    // no memory clobber: the velocity loads of the next batch may be hoisted
+    // above these reductions (they never alias the histogram); the callers
+    // fence the compiler before the histogram is read with plain loads
+    asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(hs_word + (unsigned)q * 64u), "r"(half_one));
+#endif
 #else
     (void)hs_word;
     (void)half_one;
@@ -879,6 +886,9 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
 #endif
     constexpr int U = FM_LEAN_U;
     int k = 0;
+#ifdef FM_LEAN_UNROLL2
+#pragma unroll 2
+#endif
     for (; k + U <= nk; k += U) {
         double2 v[U];
 #pragma unroll
@@ -1423,6 +1433,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                                                             S, viol);
                     }
                 }
+                asm volatile("" ::: "memory");   // histogram reductions (no clobber) before any plain access
                 __syncwarp();
             }
             const bool dead_row = row_ok && (R.rflags & RF_DEAD);
