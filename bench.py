@@ -330,11 +330,15 @@ def run_ours(args):
     flops_per_transition = 13 + 4 * w.n_modes / w.n_actions
     units_rank = (j1 - j0) * g.nx * g.nt * w.n_actions * w.n_realizations
     achieved = units_rank * flops_per_transition / (build_ms / 1e3)
-    traffic = None
+    traffic, pipe = None, {}
     prof = os.path.join(ROOT, "profiles", "k_build_paper_ncu.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.workload == WORKLOAD:
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            # one build = the lean-task and obstacle-task launches of k_build
+            traffic = pj.get("dram_bytes_all_launches", pj.get("dram_bytes_per_launch"))
+            pipe = {"ncu_fp64_pipe_pct_lean_part": pj.get("fp64_pipe_pct_first"),
+                    "ncu_issue_active_pct_lean_part": pj.get("issue_active_pct_first")}
         except Exception:
             traffic = None
 
@@ -358,7 +362,11 @@ def run_ours(args):
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": "fm_fp64_probe in this run (DADD+DMUL issue rate); MEASURED_PEAKS.json "
                                         "has no FP64 figure",
-                         "flops_per_transition": flops_per_transition},
+                         "flops_per_transition": flops_per_transition,
+                         "flops_note": "algorithmic count of SURVEY.md 8(d) (13 + 4 N_m/|A|); the kernel executes "
+                                       "fewer (identity ops skipped, floor as one DADD, count-formed rewards: "
+                                       "6 + 32/|A| FP64 per transition), see the ncu pipe figures",
+                         **pipe},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -44,6 +44,10 @@ if not launches:
 first = launches[0]
 summary = {"report": rep.split("/")[-1], "kernel_regex": kern, "note": note, "launches": len(launches),
            "dram_bytes_per_launch": first.get("dram__bytes_read.sum", 0) + first.get("dram__bytes_write.sum", 0),
+           "dram_bytes_all_launches": sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+                                          for m in launches),
+           "fp64_pipe_pct_first": first.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+           "issue_active_pct_first": first.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
            "duration_s_under_ncu": first.get("gpu__time_duration.sum"), "metrics": launches}
 json.dump(summary, open(out, "w"), indent=1)
 print(json.dumps({k: v for k, v in summary.items() if k != "metrics"}, indent=1))
