@@ -42,10 +42,19 @@ for row in r[2:]:
 if not launches:
     sys.exit(f"no launch of {kern} in {rep}")
 first = launches[0]
+
+
+def _sum_finite(ls):
+    tot = 0.0
+    for m in ls:
+        b = m.get("dram__bytes_read.sum", float("nan")) + m.get("dram__bytes_write.sum", float("nan"))
+        if not (b == b):   # a launch ncu could not replay: no total
+            return None
+        tot += b
+    return tot
 summary = {"report": rep.split("/")[-1], "kernel_regex": kern, "note": note, "launches": len(launches),
            "dram_bytes_per_launch": first.get("dram__bytes_read.sum", 0) + first.get("dram__bytes_write.sum", 0),
-           "dram_bytes_all_launches": sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
-                                          for m in launches),
+           "dram_bytes_all_launches": _sum_finite(launches),
            "fp64_pipe_pct_first": first.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
            "issue_active_pct_first": first.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
            "duration_s_under_ncu": first.get("gpu__time_duration.sum"), "metrics": launches}
