@@ -336,7 +336,7 @@ def run_ours(args):
         try:
             pj = json.load(open(prof))
             # one build = the lean-task and obstacle-task launches of k_build
-            traffic = pj.get("dram_bytes_all_launches", pj.get("dram_bytes_per_launch"))
+            traffic = pj.get("dram_bytes_all_launches") or pj.get("dram_bytes_per_launch")
             pipe = {"ncu_fp64_pipe_pct_lean_part": pj.get("fp64_pipe_pct_first"),
                     "ncu_issue_active_pct_lean_part": pj.get("issue_active_pct_first")}
         except Exception:

@@ -58,5 +58,15 @@ summary = {"report": rep.split("/")[-1], "kernel_regex": kern, "note": note, "la
            "fp64_pipe_pct_first": first.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
            "issue_active_pct_first": first.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
            "duration_s_under_ncu": first.get("gpu__time_duration.sum"), "metrics": launches}
-json.dump(summary, open(out, "w"), indent=1)
+def _clean(x):   # strict JSON: a launch ncu could not replay has NaN metrics
+    if isinstance(x, float) and x != x:
+        return None
+    if isinstance(x, dict):
+        return {k: _clean(v) for k, v in x.items()}
+    if isinstance(x, list):
+        return [_clean(v) for v in x]
+    return x
+
+
+json.dump(_clean(summary), open(out, "w"), indent=1)
 print(json.dumps({k: v for k, v in summary.items() if k != "metrics"}, indent=1))
