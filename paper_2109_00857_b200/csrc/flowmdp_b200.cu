@@ -417,6 +417,9 @@ struct BuildK {
     int hx, hy, width, nslot, hw;
     int rx, ry;
     int src_cell_exact;      // floor((x0(c) - o) / dx) == c for every cell centre
+    // F_PROVEN: source columns / rows whose transit end ex = x0 + (x1 - x0)
+    // equals x1 for every landing (Sterbenz): c >= lo or c <= hi
+    int sx_lo, sx_hi, sy_lo, sy_hi;
     const int32_t *gate_r;   // device [rx, ry] (fm_gate_radius) or null
     // task decomposition
     int t0, t1, cell0, ncell;   // strip = cells [cell0, cell0 + ncell) of each layer
@@ -1270,6 +1273,9 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                                 // tight needs cell(x0) == source cell (host-checked)
                                 c = (!K.src_cell_exact || box_count(K, t, min(cci, li), max(cci, li),
                                                                     min(ccj, lj), max(ccj, lj)) > 0) ? 2 : 3;
+                                // ex == x1 exactly for this source: the tight box is the exact one
+                                if (c == 3 && (cci >= K.sx_lo || cci <= K.sx_hi) && (ccj >= K.sy_lo || ccj <= K.sy_hi))
+                                    c = 0;
                             }
                         }
                     }
@@ -1644,6 +1650,25 @@ static bool source_cells_exact(const fm_grid &G)
     return true;
 }
 
+// Sterbenz ranges of one axis: with x1 in [fl(x0 - R), fl(x0 + R)] and
+// x1 / 2 <= x0 <= 2 x1 (same sign), x1 - x0 is exact, so x0 + (x1 - x0)
+// rounds to x1 itself.  lo = first index from which every larger index
+// qualifies (positive side), hi = last index up to which every smaller one
+// qualifies (negative side).
+static void sterbenz_axis(int n, double o, double dx, double R, int &lo, int &hi)
+{
+    auto ok = [&](int c) {
+        const double x0 = o + ((double)c + 0.5) * dx, a = x0 - R, b = x0 + R;
+        if (a > 0.0) return x0 <= 2.0 * a && b <= 2.0 * x0;
+        if (b < 0.0) return -x0 <= -2.0 * b && -a <= -2.0 * x0;
+        return false;
+    };
+    lo = n;
+    while (lo > 0 && ok(lo - 1)) --lo;
+    hi = -1;
+    while (hi + 1 < n && ok(hi + 1)) ++hi;
+}
+
 static bool prove_lean(const fm_build_args *h)
 {
     const double vx = h->vmax_x, vy = h->vmax_y;
@@ -1748,6 +1773,10 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
     K.smem_warp = align16(K.off_danger + 2 * K.CW * (int)((nslot + 31) / 32) * 4);
     K.src_cell_exact = source_cells_exact(G) ? 1 : 0;
+    K.sx_lo = G.nx;
+    K.sx_hi = -1;
+    K.sy_lo = G.ny;
+    K.sy_hi = -1;
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
     K.entries = M->entries; K.capacity = M->capacity;
     K.nnz_counter = reinterpret_cast<unsigned long long *>(M->d_nnz);
@@ -1763,6 +1792,18 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.gate_r = h->d_gate_r;
     if (h->h_actions && prove_lean(h)) {
         flags |= F_PROVEN;
+        double ax = 0.0, ay = 0.0;
+        for (int a = 0; a < h->n_actions; ++a) {
+            ax = fmax(ax, fabs(h->h_actions[a].ax));
+            ay = fmax(ay, fabs(h->h_actions[a].ay));
+        }
+        // reach bound of prove_lean, widened by a relative 2^-40 for the
+        // rounding of x0 + p (|fl(x0 + p) - (x0 + p)| <= ulp)
+        const double mx = fmax(fabs(G.ox), fabs(G.ox + G.nx * G.dx)), my = fmax(fabs(G.oy), fabs(G.oy + G.ny * G.dx));
+        const double Rx = (h->vmax_x + ax) * G.dt * (1.0 + 0x1p-40) + 0x1p-40 * mx;
+        const double Ry = (h->vmax_y + ay) * G.dt * (1.0 + 0x1p-40) + 0x1p-40 * my;
+        sterbenz_axis(G.nx, G.ox, G.dx, Rx, K.sx_lo, K.sx_hi);
+        sterbenz_axis(G.ny, G.oy, G.dx, Ry, K.sy_lo, K.sy_hi);
         if (K.obj != FM_OBJ_NET_ENERGY && rewards_sum_exactly(h)) flags |= F_CNT;
     }
     return FM_OK;
