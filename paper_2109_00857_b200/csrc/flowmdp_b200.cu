@@ -867,8 +867,7 @@ __device__ __forceinline__ void hist_inc(uint16_t *h16q, unsigned hs_word, int q
 #endif
 #else
     (void)hs_word;
-    (void)half_one;
-    h16q[q * 32] += (uint16_t)1;
+    h16q[q * 32] += (uint16_t)(half_one ? 1 : 0);
 #endif
 }
 
@@ -946,12 +945,10 @@ __device__ __forceinline__ int obst_slot(const BuildK &K, const RowC &R, const d
     const int j1 = floor_magic(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx));
     const int q = j1 * K.width + i1, slot = q + R.soff;
     const int c = (int)((cls[slot >> 4] >> ((slot & 15) << 1)) & 3u);   // see fast_transition
-    rare = c == 2;
-    if (c == 3) {
-        const double ex = DADD(R.x0, DSUB(x1, R.x0)), ey = DADD(R.y0, DSUB(y1, R.y0));
-        rare = floor_magic(to_cell<FLAGS>(ex, K.ox, K.dx, K.inv_dx)) != i1 ||
-               floor_magic(to_cell<FLAGS>(ey, K.oy, K.dx, K.inv_dx)) != j1;
-    }
+    // classes 2 and 3 are deferred to the exact sampling (for class 3 the
+    // box prefilter would mostly clear it, but the few class-3 slots left
+    // after the Sterbenz downgrade are not worth a branch per transition)
+    rare = c >= 2;
     return c == 1 ? outq : q;
 }
 
@@ -986,11 +983,12 @@ __device__ __forceinline__ void chunk_rows_obst_cnt(const BuildK *__restrict__ K
         for (int u = 0; u < 4; ++u) v[u] = vrow[k + u];
 #pragma unroll
         for (int u = 0; u < 4; ++u) q[u] = obst_slot<FLAGS>(K, R, v[u], cls, outq, r[u]);
+        // branch-free: a deferred transition adds 0 now (its slot is settled
+        // in the drain); the batch's deferral bits enter the mask at once
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (r[u]) pend |= 1ull << ((k + u) & 63);
-            else hist_inc(h16q, hs_word, q[u], half_one);
-        }
+        for (int u = 0; u < 4; ++u) hist_inc(h16q, hs_word, q[u], r[u] ? 0u : half_one);
+        const unsigned bits = (r[0] ? 1u : 0u) | (r[1] ? 2u : 0u) | (r[2] ? 4u : 0u) | (r[3] ? 8u : 0u);
+        pend |= (unsigned long long)bits << (k & 63);
     }
     for (; k < nk; ++k) {
         bool r0;
