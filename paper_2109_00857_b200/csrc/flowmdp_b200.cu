@@ -179,46 +179,63 @@ __device__ __forceinline__ float2 ffma2_bcast(float a, float2 b, float2 c)
     return *reinterpret_cast<float2 *>(&r);
 }
 
+// Each thread scans two cells (c, c + 256) so every staged coefficient feeds
+// two FFMA2 chains; the running exact maxima are shared by the two cells
+// (an element can only raise the global maximum if |v32| >= E - delta_cell).
+static constexpr int kVmaxCells = 2;
+
 template <int NMX>
 __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_block, const double *cmax, double *out2)
 {
     __shared__ float cs[kVmaxChunk][NMX];
     const int nc = G.nx * G.ny;
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int t = blockIdx.y;
     const int nm = E.n_modes;
     const int r_lo = blockIdx.z * r_per_block;
     const int r_hi = min(E.n_real, r_lo + r_per_block);
-    const bool ok = c < nc;
-    float mx32 = 0.f, my32 = 0.f;
-    float dx32[NMX], dy32[NMX];
-    float2 d32[NMX];
-    double Tx = 0.0, Ty = 0.0;
-    if (ok) {
-        const double2 mu = *reinterpret_cast<const double2 *>(E.mean + ((size_t)t * nc + c) * 2);
-        mx32 = (float)mu.x;
-        my32 = (float)mu.y;
-        Tx = fabs(mu.x);
-        Ty = fabs(mu.y);
+    int cell[kVmaxCells];
+    bool ok[kVmaxCells];
+    float2 mu32[kVmaxCells];
+    float2 d32[kVmaxCells][NMX];
+    double delx[kVmaxCells], dely[kVmaxCells];
 #pragma unroll
-        for (int m = 0; m < NMX; ++m) {
-            dx32[m] = dy32[m] = 0.f;
-            d32[m] = make_float2(0.f, 0.f);
-            if (m < nm) {
-                const double2 md = *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + c) * 2);
-                dx32[m] = (float)md.x;
-                dy32[m] = (float)md.y;
-                d32[m] = make_float2(dx32[m], dy32[m]);
-                const double cm = cmax[(size_t)t * nm + m];
-                Tx += fabs(md.x) * cm;
-                Ty += fabs(md.y) * cm;
+    for (int q = 0; q < kVmaxCells; ++q) {
+        const int c = blockIdx.x * blockDim.x * kVmaxCells + q * blockDim.x + threadIdx.x;
+        cell[q] = c;
+        ok[q] = c < nc;
+        mu32[q] = make_float2(0.f, 0.f);
+        double Tx = 0.0, Ty = 0.0;
+#pragma unroll
+        for (int m = 0; m < NMX; ++m) d32[q][m] = make_float2(0.f, 0.f);
+        if (ok[q]) {
+            const double2 mu = *reinterpret_cast<const double2 *>(E.mean + ((size_t)t * nc + c) * 2);
+            mu32[q] = make_float2((float)mu.x, (float)mu.y);
+            Tx = fabs(mu.x);
+            Ty = fabs(mu.y);
+#pragma unroll
+            for (int m = 0; m < NMX; ++m) {
+                if (m < nm) {
+                    const double2 md =
+                        *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + c) * 2);
+                    d32[q][m] = make_float2((float)md.x, (float)md.y);
+                    const double cm = cmax[(size_t)t * nm + m];
+                    Tx += fabs(md.x) * cm;
+                    Ty += fabs(md.y) * cm;
+                }
             }
         }
+        const double kRel = (2.0 * nm + 8.0) * 0x1p-24 * 1.001, kAbs = (nm + 2.0) * 0x1p-140;
+        delx[q] = Tx * kRel + kAbs;
+        dely[q] = Ty * kRel + kAbs;
     }
-    const double kRel = (2.0 * nm + 8.0) * 0x1p-24 * 1.001, kAbs = (nm + 2.0) * 0x1p-140;
-    const double delx = Tx * kRel + kAbs, dely = Ty * kRel + kAbs;
-    double ex = 0.0, ey = 0.0;                                    // running exact maxima
-    float thx = __double2float_rd(-delx), thy = __double2float_rd(-dely);
+    double ex = 0.0, ey = 0.0;   // running exact maxima (shared by this thread's cells)
+    float thx[kVmaxCells], thy[kVmaxCells];
+#pragma unroll
+    for (int q = 0; q < kVmaxCells; ++q) {
+        // a cell past the grid never passes: its threshold is +inf
+        thx[q] = ok[q] ? __double2float_rd(-delx[q]) : __int_as_float(0x7f800000);
+        thy[q] = ok[q] ? __double2float_rd(-dely[q]) : __int_as_float(0x7f800000);
+    }
     for (int r0 = r_lo; r0 < r_hi; r0 += kVmaxChunk) {
         const int n = min(kVmaxChunk, r_hi - r0);
         __syncthreads();
@@ -227,36 +244,52 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_blo
             cs[k][m] = m < nm ? (float)E.coeffs[((size_t)t * E.n_real + r0 + k) * nm + m] : 0.f;
         }
         __syncthreads();
-        if (!ok) continue;
+        if (!ok[0]) continue;
         // two realizations per step; (vx, vy) in one packed FFMA2 chain.
         // Unused modes hold zeros (exact no-ops), so no mode-count test.
         // chunks hold an even count except possibly the last (n odd: the
         // second lane of the pair re-evaluates realization k, harmless)
         for (int k = 0; k < n; k += 2) {
             const int k1 = k + 1 < n ? k + 1 : k;
-            float2 v0 = make_float2(mx32, my32), v1 = v0;
+            float2 v0[kVmaxCells], v1[kVmaxCells];
+#pragma unroll
+            for (int q = 0; q < kVmaxCells; ++q) v0[q] = v1[q] = mu32[q];
 #pragma unroll
             for (int m = 0; m < NMX; ++m) {
-                v0 = ffma2_bcast(cs[k][m], d32[m], v0);
-                v1 = ffma2_bcast(cs[k1][m], d32[m], v1);
+                const float c0 = cs[k][m], c1 = cs[k1][m];
+#pragma unroll
+                for (int q = 0; q < kVmaxCells; ++q) {
+                    v0[q] = ffma2_bcast(c0, d32[q][m], v0[q]);
+                    v1[q] = ffma2_bcast(c1, d32[q][m], v1[q]);
+                }
             }
             // !(|v| < th) also routes NaN / inf to the exact path
-            const bool hit = !(fabsf(v0.x) < thx) || !(fabsf(v0.y) < thy) || !(fabsf(v1.x) < thx) ||
-                             !(fabsf(v1.y) < thy);
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < kVmaxCells; ++q)
+                hit = hit || !(fabsf(v0[q].x) < thx[q]) || !(fabsf(v0[q].y) < thy[q]) ||
+                      !(fabsf(v1[q].x) < thx[q]) || !(fabsf(v1[q].y) < thy[q]);
             if (hit) {
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const float2 v = j ? v1 : v0;
-                    const int r = r0 + (j ? k1 : k);
-                    if (!(fabsf(v.x) < thx)) {
-                        const double e = vmax_exact_component<NMX>(G, E, t, r, c, 0);
-                        ex = (e != e || e > ex) ? e : ex;   // NaN sticks (the reference's max propagates it)
-                        thx = __double2float_rd(ex - delx);
-                    }
-                    if (!(fabsf(v.y) < thy)) {
-                        const double e = vmax_exact_component<NMX>(G, E, t, r, c, 1);
-                        ey = (e != e || e > ey) ? e : ey;
-                        thy = __double2float_rd(ey - dely);
+                for (int q = 0; q < kVmaxCells; ++q) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const float2 v = j ? v1[q] : v0[q];
+                        const int r = r0 + (j ? k1 : k);
+                        if (!(fabsf(v.x) < thx[q])) {
+                            const double e = vmax_exact_component<NMX>(G, E, t, r, cell[q], 0);
+                            ex = (e != e || e > ex) ? e : ex;   // NaN sticks (the reference's max propagates it)
+#pragma unroll
+                            for (int qq = 0; qq < kVmaxCells; ++qq)
+                                if (ok[qq]) thx[qq] = __double2float_rd(ex - delx[qq]);
+                        }
+                        if (!(fabsf(v.y) < thy[q])) {
+                            const double e = vmax_exact_component<NMX>(G, E, t, r, cell[q], 1);
+                            ey = (e != e || e > ey) ? e : ey;
+#pragma unroll
+                            for (int qq = 0; qq < kVmaxCells; ++qq)
+                                if (ok[qq]) thy[qq] = __double2float_rd(ey - dely[qq]);
+                        }
                     }
                 }
             }
@@ -297,7 +330,7 @@ extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *st
         k_maxabs_seg<<<G.nt * nm, 256, 0, s>>>(E.coeffs, E.n_real, nm, nm, (int64_t)E.n_real * nm, 1, cmax);
         FM_CK_LAUNCH("k_maxabs_seg");
     }
-    const int bx = (nc + 255) / 256;
+    const int bx = (nc + 256 * kVmaxCells - 1) / (256 * kVmaxCells);
     long long base = (long long)bx * G.nt;
     int rpb = E.n_real;
     const long long want = 4LL * sm_count();
