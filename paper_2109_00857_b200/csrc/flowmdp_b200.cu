@@ -29,6 +29,11 @@
 
 static constexpr unsigned kFull = 0xffffffffu;
 
+// realizations per reconstruction chunk of k_build
+#ifndef FM_BUILD_RC
+#define FM_BUILD_RC 64
+#endif
+
 // ---------------------------------------------------------------------------
 // error plumbing
 // ---------------------------------------------------------------------------
@@ -921,6 +926,29 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
 #endif
     constexpr int U = FM_LEAN_U;
     int k = 0;
+#ifndef FM_LEAN_NO_FULL
+    if (nk == FM_BUILD_RC) {
+        // full chunk: the batch loop unrolled (no loop-carried branch; the
+        // scheduler may interleave consecutive batches)
+#pragma unroll
+        for (int kb = 0; kb < FM_BUILD_RC; kb += U) {
+            double2 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = vrow[kb + u];
+            int q[U];
+            double w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) q[u] = lean_transition<FLAGS, EDGE>(K, R, v[u], g_n, outq, w[u]);
+            if (!(FLAGS & F_CNT)) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) S = DADD(S, w[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) hist_inc(h16q, hs_word, q[u], half_one);
+        }
+        return;
+    }
+#endif
 #ifdef FM_LEAN_UNROLL2
 #pragma unroll 2
 #endif
@@ -1158,9 +1186,6 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
 //   other part's tasks.
 #ifndef FM_BUILD_MINB
 #define FM_BUILD_MINB 4
-#endif
-#ifndef FM_BUILD_RC
-#define FM_BUILD_RC 64
 #endif
 static_assert(FM_BUILD_RC <= 64, "chunk_rows_obst_cnt marks deferred realizations in a 64-bit mask");
 template <int FLAGS, int PART>
@@ -1583,6 +1608,20 @@ __global__ void k_viol_report(const __grid_constant__ BuildK K, int t, int a, in
 
 static int align16(int x) { return (x + 15) & ~15; }
 
+// Per-warp shared memory: u16 histogram [nslot+1][32] | v chunk [CW][RC+1]
+// | transposed coefficients [nm][RC] | modes [CW][nm] | danger classes
+// [CW][2 words per 32 slots] | (queue entries) deferred exact tests.
+static void smem_layout(BuildK &K, int RC, int queue)
+{
+    K.RC = RC;
+    K.off_vbuf = align16((K.nslot + 1) * 64);
+    K.off_coef = K.off_vbuf + K.CW * (K.RC + 1) * (int)sizeof(double2);
+    K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
+    K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
+    K.off_queue = align16(K.off_danger + 2 * K.CW * ((K.nslot + 31) / 32) * 4);
+    K.smem_warp = align16(K.off_queue + queue * (int)sizeof(QItem));
+}
+
 template <int FL, int PART>
 static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
 {
@@ -1607,9 +1646,9 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
         if (st != FM_OK) return st;
         if constexpr ((FL & F_CNT) != 0) {
             // obstacle part: per-warp queue of deferred exact segment tests
+            // (half-size reconstruction chunks keep it at 4 blocks per SM)
             BuildK K2 = K;
-            K2.off_queue = K.smem_warp;
-            K2.smem_warp = align16(K.smem_warp + kQueue * (int)sizeof(QItem));
+            smem_layout(K2, K.RW >= 32 ? K.RW : 32, kQueue);
             return launch_build_p<FL, 2>(K2, (size_t)4 * K2.smem_warp, s);
         } else {
             return launch_build_p<FL, 2>(K, smem, s);
@@ -1795,14 +1834,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.n_tasks = (long long)(h->t1 - h->t0) * K.groups * K.nag;
     if (K.n_tasks > 0xFFFFFFF0LL) return fm_fail(FM_BAD_ARG, "fm_build: too many tasks");
     // realizations per chunk: RW recon lanes per cell, 64 realizations
-    K.RC = K.RW >= FM_BUILD_RC ? K.RW : FM_BUILD_RC;
-    // per-warp shared memory: u16 histogram [nslot+1][32] | v chunk [CW][RC+1]
-    // | transposed coefficients [nm][RC] | modes [CW][nm]
-    K.off_vbuf = align16((int)(nslot + 1) * 64);
-    K.off_coef = K.off_vbuf + K.CW * (K.RC + 1) * (int)sizeof(double2);
-    K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
-    K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
-    K.smem_warp = align16(K.off_danger + 2 * K.CW * (int)((nslot + 31) / 32) * 4);
+    smem_layout(K, K.RW >= FM_BUILD_RC ? K.RW : FM_BUILD_RC, 0);
     K.src_cell_exact = source_cells_exact(G) ? 1 : 0;
     K.sx_lo = G.nx;
     K.sx_hi = -1;
