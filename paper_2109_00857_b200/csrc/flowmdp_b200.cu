@@ -905,7 +905,7 @@ __device__ __forceinline__ void hist_inc(uint16_t *h16q, unsigned hs_word, int q
 #endif
 #else
     (void)hs_word;
-    h16q[q * 32] += (uint16_t)(half_one ? 1 : 0);
+    h16q[q * 32] += (uint16_t)((half_one & 0xFFFFu) | (half_one >> 16));   // the increment, whichever half
 #endif
 }
 
@@ -927,7 +927,9 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
     constexpr int U = FM_LEAN_U;
     int k = 0;
 #ifndef FM_LEAN_NO_FULL
-    if (nk == FM_BUILD_RC) {
+    // (count-formed rewards only: with a per-transition reward chain the
+    // unrolled chunk spills)
+    if ((FLAGS & F_CNT) && nk == FM_BUILD_RC) {
         // full chunk: the batch loop unrolled (no loop-carried branch; the
         // scheduler may interleave consecutive batches)
 #pragma unroll
@@ -1114,6 +1116,79 @@ __device__ __forceinline__ void chunk_rows_obst_cnt(const BuildK *__restrict__ K
         __syncwarp();
     }
 #endif
+}
+
+// Obstacle-warp realization loop under F_PROVEN without F_CNT (net_energy,
+// or time / energy with non-dyadic rewards): the reward sum must follow the
+// reference's realization order, so exact segment tests run in place.
+// Branch-free slot classes; landings outside the domain, on a cell masked at
+// t+1 or through a blocked transit are bad (SINK, r_outbound); dead rows
+// send every realization to SINK (no overflow test is needed under
+// F_PROVEN).  model_builder.py:331-360, 445-458; environment.py:338-368.
+template <int FLAGS>
+__device__ __forceinline__ void chunk_rows_obst_seq(const BuildK *__restrict__ Kg, int t, const RowC &R,
+                                                    const double2 *vrow, int nk, const double *__restrict__ g_n,
+                                                    const uint32_t *cls, uint16_t *h16q, int outq, unsigned rowmask,
+                                                    double &S, unsigned half_one)
+{
+    const BuildK &K = *Kg;
+    const unsigned hs_word = (unsigned)__cvta_generic_to_shared(h16q) & ~3u;
+    const unsigned live = __ballot_sync(rowmask, !(R.rflags & RF_DEAD));
+    if (R.rflags & RF_DEAD) {
+        const double rw = (R.rflags & RF_TERMINAL) ? 0.0 : K.r_out;
+        for (int k = 0; k < nk; ++k) S = DADD(S, rw);   // ascending realization order
+        if (nk > 0) hist_inc(h16q, hs_word, outq, half_one * (unsigned)nk);
+        return;
+    }
+    int k = 0;
+    for (; k < nk; k += 4) {
+        const int nb = nk - k < 4 ? nk - k : 4;
+        double x1[4], y1[4];
+        int q[4], cell[4];
+        bool bad[4], rare[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double2 v = vrow[k + (u < nb ? u : 0)];
+            double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt  (model_builder.py:332)
+            if (!(FLAGS & F_DT_ONE)) {
+                px = DMUL(px, K.dt);
+                py = DMUL(py, K.dt);
+            }
+            x1[u] = DADD(R.x0, px);
+            y1[u] = DADD(R.y0, py);
+            const int i1 = floor_magic(to_cell<FLAGS>(x1[u], K.ox, K.dx, K.inv_dx));
+            const int j1 = floor_magic(to_cell<FLAGS>(y1[u], K.oy, K.dx, K.inv_dx));
+            q[u] = j1 * K.width + i1;
+            cell[u] = j1 * K.nx + i1;
+            const bool out = (unsigned)i1 >= (unsigned)K.nx || (unsigned)j1 >= (unsigned)K.ny;
+            const int slot = q[u] + R.soff;   // inside the window (F_PROVEN)
+            const int c = out ? 0 : (int)((cls[slot >> 4] >> ((slot & 15) << 1)) & 3u);
+            bad[u] = out || c == 1;
+            rare[u] = u < nb && c >= 2;
+        }
+        if (!__all_sync(live, !(rare[0] || rare[1] || rare[2] || rare[3]))) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (rare[u]) bad[u] = seg_samples_blocked<FLAGS>(K, t, R.x0, R.y0, x1[u], y1[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (u >= nb) break;
+            const bool hit = !bad[u] && q[u] == R.tslot;
+            double rw;
+            if (FLAGS & F_NET) {
+                const double gd = bad[u] ? 0.0 : __ldg(g_n + cell[u]);
+                double b = DADD(R.AB, DMUL(K.h_cr, gd));
+                if (!(FLAGS & F_DT_ONE)) b = DMUL(b, K.dt);
+                rw = hit ? DADD(b, K.r_term) : b;
+            } else {
+                rw = hit ? R.base_hit : R.base;
+            }
+            if (bad[u]) rw = K.r_out;
+            S = DADD(S, rw);   // ascending realization order (model_builder.py:457-458)
+            hist_inc(h16q, hs_word, bad[u] ? outq : q[u], half_one);
+        }
+    }
 }
 
 // The realization loop of one chunk for the row lanes: 4 independent
@@ -1466,6 +1541,9 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                     chunk_rows_obst_cnt<FLAGS>(Kg, t, Rf, vrow, nk, cls, h16q, outq,
                                                row_ok && !(R.rflags & RF_DEAD), half_one, wbase + K.off_queue,
                                                (unsigned)__cvta_generic_to_shared(hist16), grp);
+                } else if ((FLAGS & F_PROVEN) && obst) {
+                    if (row_ok) chunk_rows_obst_seq<FLAGS>(Kg, t, Rf, vrow, nk, g_n, cls, h16q, outq, rowmask, S,
+                                                           half_one);
                 } else if (row_ok) {
                     FM_STAT(obst ? 3 : 4, nk);
                     if (obst) {
