@@ -466,6 +466,7 @@ struct BuildK {
     // per-warp shared-memory carve-up (bytes)
     int smem_warp, off_vbuf, off_coef, off_modes, off_danger;
     int off_queue;   // PART 2 (F_PROVEN | F_CNT): deferred exact-test queue [kQueue]
+    int off_hg;      // PART 1 (F_PROVEN | F_NET): h_cr * g[t+1] per (cell, window slot)
     // outputs
     uint64_t *row_ptr;
     uint16_t *row_nnz;
@@ -826,7 +827,10 @@ __device__ __forceinline__ void recon_m8(const double2 *md, const double2 *c2, d
 #pragma unroll
     for (int i = 0; i < 8; ++i) m[i] = md[i];
     for (int p = 0; p < RPL; p += 2) {
-        const int rl0 = p * RW + rr, rl1 = p + 1 < RPL ? rl0 + RW : rl0;   // odd RPL: recompute rl0
+        // odd RPL recomputes rl0; realizations past the chunk (RW not dividing
+        // RC) read a valid coefficient and are not stored
+        const int rl0 = p * RW + rr < RC ? p * RW + rr : RC - 1;
+        const int rl1 = p + 1 < RPL && rl0 + RW < RC ? rl0 + RW : rl0;
         double x0 = mu.x, y0 = mu.y, x1 = mu.x, y1 = mu.y;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -840,7 +844,7 @@ __device__ __forceinline__ void recon_m8(const double2 *md, const double2 *c2, d
             x1 = DADD(x1, DMUL(k1.y, m[2 * q + 1].x));
             y1 = DADD(y1, DMUL(k1.y, m[2 * q + 1].y));
         }
-        if (rl0 < n_left) vout[rl0] = make_double2(x0, y0);
+        if (p * RW + rr < RC && rl0 < n_left) vout[rl0] = make_double2(x0, y0);
         if (rl1 != rl0 && rl1 < n_left) vout[rl1] = make_double2(x1, y1);
     }
 }
@@ -859,6 +863,10 @@ __device__ __forceinline__ int lean_transition(const BuildK &K, const RowC &R, c
     const int i1 = floor_magic(to_cell<FLAGS>(DADD(R.x0, px), K.ox, K.dx, K.inv_dx));
     const int j1 = floor_magic(to_cell<FLAGS>(DADD(R.y0, py), K.oy, K.dx, K.inv_dx));
     int q = j1 * K.width + i1;
+    // net energy: g_n here is the warp's table h_cr * g[t+1][landing cell]
+    // per window slot, shifted by soff (0 for cells outside the domain); read
+    // at the window slot, which exists for every landing under F_PROVEN
+    const double hg = (FLAGS & F_NET) ? g_n[q] : 0.0;
     bool out = false;
     if (EDGE) {
         out = (unsigned)i1 >= (unsigned)K.nx || (unsigned)j1 >= (unsigned)K.ny;
@@ -867,8 +875,7 @@ __device__ __forceinline__ int lean_transition(const BuildK &K, const RowC &R, c
     if (!(FLAGS & F_CNT)) {
         const bool hit = q == R.tslot;
         if (FLAGS & F_NET) {
-            const double gd = __ldg(g_n + (out ? 0 : j1 * K.nx + i1));
-            double b = DADD(R.AB, DMUL(K.h_cr, gd));
+            double b = DADD(R.AB, hg);
             if (!(FLAGS & F_DT_ONE)) b = DMUL(b, K.dt);
             rw = hit ? DADD(b, K.r_term) : b;
         } else {
@@ -1280,7 +1287,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
     for (int sl = 0; sl <= K.nslot; ++sl) h16[sl * 32] = 0;
 
     const int AG = K.AG, RW = K.RW, CW = K.CW, nm = K.nm, nr = K.nr;
-    const int RC = K.RC, RPL = RC / RW;
+    const int RC = K.RC, RPL = (RC + RW - 1) / RW;   // RW need not divide RC (e.g. |A| = 6: RW = 6)
     const int cs_row = lane / AG, a_loc = lane - cs_row * AG;
     const bool row_lane = lane < CW * AG;
     const int cs_rec = lane / RW, rr = lane - cs_rec * RW;
@@ -1450,6 +1457,25 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
             // even mode count and 16-byte aligned coefficient rows: pair layout
             const bool pairs = (nm & 1) == 0 && nm > 0 && ((reinterpret_cast<uintptr_t>(cf_t) & 15) == 0);
             const double *g_n = K.g + (size_t)(t + 1) * K.nc;
+            // lean net-energy rows: table h_cr * g[t+1][landing cell] per
+            // (cell, window slot), 0 outside the domain (model_builder.py:357-358)
+            const double *hgq = g_n;
+            if ((FLAGS & F_NET) && (FLAGS & F_PROVEN) && PART == 1) {
+                double *hg = reinterpret_cast<double *>(wbase + K.off_hg);
+                for (int i = lane; i < CW * nslot; i += 32) {
+                    const int cs = i / nslot, sl = i - cs * nslot;
+                    const int lc = grp * CW + cs;
+                    double hv = 0.0;
+                    if (lc < K.ncell) {
+                        const int cc = K.cell0 + lc;
+                        const int li = cc % K.nx + sl % W - K.hx, lj = cc / K.nx + sl / W - K.hy;
+                        if ((unsigned)li < (unsigned)K.nx && (unsigned)lj < (unsigned)K.ny)
+                            hv = DMUL(K.h_cr, g_n[lj * K.nx + li]);
+                    }
+                    hg[i] = hv;
+                }
+                hgq = hg + cs_row * nslot + R.soff;   // indexed by q = slot - soff
+            }
             const double2 *vrow = vbuf + cs_row * (RC + 1);
             // chunk loader: coefficients [r0, r0+RC) x [0, nm) land transposed
             // as coefT[m][r - r0] (conflict-free reads in the reconstruction);
@@ -1507,7 +1533,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                     const double2 *md = modes_s + cs_rec * nm;
                     for (int p = 0; p < RPL; ++p) {
                         const int rl = p * RW + rr;
-                        if (r0 + rl < nr) {
+                        if (rl < RC && r0 + rl < nr) {
                             double vx = mu.x, vy = mu.y;
                             if (pairs) {
                                 const double2 *c2 = reinterpret_cast<const double2 *>(coefT) + rl;
@@ -1561,9 +1587,9 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
 #else
                         if (edge && !(FLAGS & F_CNT))
 #endif
-                            chunk_rows_lean<FLAGS, true>(K, Rf, vrow, nk, g_n, h16q, outq, S, half_one);
+                            chunk_rows_lean<FLAGS, true>(K, Rf, vrow, nk, hgq, h16q, outq, S, half_one);
                         else
-                            chunk_rows_lean<FLAGS, false>(K, Rf, vrow, nk, g_n, h16q, outq, S, half_one);
+                            chunk_rows_lean<FLAGS, false>(K, Rf, vrow, nk, hgq, h16q, outq, S, half_one);
                     } else {
                         if (edge)
                             chunk_rows<FLAGS, true, false>(K, Kg, t, Rf, vrow, nk, g_n, cls, h16q, outq, rowmask, S,
@@ -1689,7 +1715,7 @@ static int align16(int x) { return (x + 15) & ~15; }
 // Per-warp shared memory: u16 histogram [nslot+1][32] | v chunk [CW][RC+1]
 // | transposed coefficients [nm][RC] | modes [CW][nm] | danger classes
 // [CW][2 words per 32 slots] | (queue entries) deferred exact tests.
-static void smem_layout(BuildK &K, int RC, int queue)
+static void smem_layout(BuildK &K, int RC, int queue, bool hg = false)
 {
     K.RC = RC;
     K.off_vbuf = align16((K.nslot + 1) * 64);
@@ -1697,7 +1723,8 @@ static void smem_layout(BuildK &K, int RC, int queue)
     K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
     K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
     K.off_queue = align16(K.off_danger + 2 * K.CW * ((K.nslot + 31) / 32) * 4);
-    K.smem_warp = align16(K.off_queue + queue * (int)sizeof(QItem));
+    K.off_hg = align16(K.off_queue + queue * (int)sizeof(QItem));
+    K.smem_warp = align16(K.off_hg + (hg ? K.CW * K.nslot * (int)sizeof(double) : 0));
 }
 
 template <int FL, int PART>
@@ -1720,7 +1747,16 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
     if constexpr (!(FL & F_PROVEN)) {
         return launch_build_p<FL, 0>(K, smem, s);
     } else {
-        const int32_t st = launch_build_p<FL, 1>(K, smem, s);
+        int32_t st;
+        if constexpr ((FL & F_NET) != 0) {
+            // lean net-energy rows read h_cr * g[t+1] from a per-warp slot
+            // table (half-size chunks keep 4 blocks per SM)
+            BuildK K1 = K;
+            smem_layout(K1, K.RW >= 32 ? K.RW : 32, 0, true);
+            st = launch_build_p<FL, 1>(K1, (size_t)4 * K1.smem_warp, s);
+        } else {
+            st = launch_build_p<FL, 1>(K, smem, s);
+        }
         if (st != FM_OK) return st;
         if constexpr ((FL & F_CNT) != 0) {
             // obstacle part: per-warp queue of deferred exact segment tests

@@ -341,3 +341,15 @@ def test_wide_action_sets_parity(heads):
     for obj in ("time", "net_energy"):
         rcfg = RewardConfig(obj, c_f=1.0, c_r=0.5, r_term=100.0, r_outbound=-300.0)
         _gpu_case(env, acts, rcfg, target)
+
+
+@pytest.mark.parametrize("heads,speeds", [(3, 1), (5, 1), (3, 2), (7, 1)])
+def test_action_counts_not_dividing_a_warp(heads, speeds):
+    """|A| = 3, 5, 6, 7: several source cells per warp with a reconstruction
+    lane count that does not divide the realization chunk (500 realizations
+    span several chunks), time and net_energy, every block vs the oracle."""
+    env, _, _, target, _ = make_named_env("desk")
+    acts = ActionSpace(n_headings=heads, n_speeds=speeds, f_max=1.0)
+    for obj in ("time", "net_energy"):
+        rcfg = RewardConfig(obj, c_f=1.0, c_r=0.5, r_term=100.0, r_outbound=-300.0)
+        _gpu_case(env, acts, rcfg, target)
