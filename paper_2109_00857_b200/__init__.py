@@ -7,7 +7,10 @@ Drop-in for the hot path of the reference package ``flowmdp``:
     policy_value                          (solver.py:75, :112, :122)
 
 with the reference's value types and errors, plus the device-resident
-planner ``plan`` (build + backward solve without leaving HBM).  The compute
+planner ``plan`` (build + backward solve without leaving HBM), and the
+stages around it: ``ensemble_rollout`` / ``simulate_trajectory``
+(rollout.py), ``reduce_order`` (synthesis.py), the stage files (``io``) and
+the file pipeline (``pipeline``).  The compute
 runs in hand-written sm_100a CUDA (csrc/flowmdp_b200.cu) behind the C ABI
 in include/flowmdp_b200.h; there is no CPU fallback.
 """
@@ -42,6 +45,8 @@ from .errors import (
 from .builder import DeviceEnv, DeviceModel, build_device_model, build_model, compute_subgrid
 from .solver import extract_policy, policy_value, solve_backward, value_iteration
 from .planner import Plan, plan
+from .order import reduce_order
+from .rollout import Trajectory, TrajectoryEnsemble, ensemble_rollout, simulate_trajectory
 
 __all__ = [
     "OUTSIDE", "ActionSpace", "CooBlock", "DOVelocityField", "Environment", "GridSpec", "ObstacleMask",
@@ -52,4 +57,5 @@ __all__ = [
     "DeviceEnv", "DeviceModel", "build_device_model", "build_model", "compute_subgrid",
     "extract_policy", "policy_value", "solve_backward", "value_iteration",
     "Plan", "plan",
+    "reduce_order", "Trajectory", "TrajectoryEnsemble", "ensemble_rollout", "simulate_trajectory",
 ]

@@ -158,6 +158,7 @@ def main():
 
     out["pipeline"] = pipeline_records(fm)
     out["rollout"] = rollout_records(fm, conf)
+    order_fixture(fm)
     os.makedirs(os.path.dirname(GOLDEN_JSON), exist_ok=True)
     with open(GOLDEN_JSON, "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
@@ -231,6 +232,20 @@ def rollout_records(fm, conf):
     return recs
 
 
+def order_fixture(fm):
+    """Reference reduce_order on a seeded low-rank-plus-noise ensemble; the
+    outputs are stored as arrays (the GPU SVD agrees to rounding, not bits)."""
+    from flowmdp.synthesis import reduce_order
+    rng = np.random.default_rng(2109)
+    n_real, nt, ny, nx, rank = 24, 3, 5, 6, 6
+    basis = rng.normal(size=(rank, nt, ny, nx, 2)) * np.linspace(3.0, 0.5, rank)[:, None, None, None, None]
+    weights = rng.normal(size=(n_real, rank))
+    ens = np.einsum("rk,ktyxc->rtyxc", weights, basis) + 1e-3 * rng.normal(size=(n_real, nt, ny, nx, 2)) + 0.7
+    field = reduce_order(ens, 4)
+    np.savez_compressed(os.path.join(os.path.dirname(GOLDEN_JSON), "reduce_order.npz"), ensemble=ens,
+                        mean=field.mean, modes=field.modes, coeffs=field.coeffs)
+
+
 def _built(fm, env, acts, rcfg, target):
     from flowmdp.model_builder import StepContext, build_model, compute_subgrid
     ctx = StepContext(env, acts, rcfg, target)
@@ -238,11 +253,16 @@ def _built(fm, env, acts, rcfg, target):
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "--pipeline-only":
+    if len(sys.argv) > 1 and sys.argv[1] == "--order-only":
+        fm_, _c = _import_reference()
+        order_fixture(fm_)
+        print("wrote reduce_order.npz")
+    elif len(sys.argv) > 1 and sys.argv[1] == "--pipeline-only":
         fm_, conf_ = _import_reference()
         gold = json.load(open(GOLDEN_JSON))
         gold["pipeline"] = pipeline_records(fm_)
         gold["rollout"] = rollout_records(fm_, conf_)
+        order_fixture(fm_)
         with open(GOLDEN_JSON, "w") as fh:
             json.dump(gold, fh, indent=1, sort_keys=True)
         print("updated", GOLDEN_JSON)
