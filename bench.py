@@ -337,6 +337,9 @@ def run_ours(args):
             pj = json.load(open(prof))
             # one build = the lean-task and obstacle-task launches of k_build
             traffic = pj.get("dram_bytes_all_launches") or pj.get("dram_bytes_per_launch")
+            p2 = os.path.join(ROOT, "profiles", "k_build_obstacle_paper_ncu.json")
+            if os.path.exists(p2):   # the obstacle-task launch of the same build
+                traffic = (traffic or 0) + (json.load(open(p2)).get("dram_bytes_per_launch") or 0)
             pipe = {"ncu_fp64_pipe_pct_lean_part": pj.get("fp64_pipe_pct_first"),
                     "ncu_issue_active_pct_lean_part": pj.get("issue_active_pct_first")}
         except Exception:
