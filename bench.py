@@ -224,7 +224,9 @@ def run_ours(args):
 
     def step(de):
         de.reset_derived()                       # sub-grid and gate statistics are recomputed every step
-        vm = de.velocity_max()                   # k_vmax (the one host round trip before the build)
+        # k_vmax over this rank's strip (+ a MAX all-reduce across ranks):
+        # the one host round trip before the build
+        vm = de.velocity_max(j_range=(j0, j1)) if world > 1 else de.velocity_max()
         sub = subgrid_from_vmax(vm, acts.f_max, g, w.buffer)
         b0, b1 = ev(), ev()
         b0.record()

@@ -144,6 +144,10 @@ int64_t fm_kernel_launches(void);
  * max |v_x|, max |v_y| over every (t, realization, cell) with the
  * reconstruction order of environment.py:293-297.  d_out2 must be zeroed. */
 int32_t fm_velocity_max(fm_grid grid, fm_env env, double *d_out2, void *stream);
+/* The same scan over the cells of rows [j0, j1) only (one GPU's strip: the
+ * global maximum is the max over strips, e.g. an all-reduce). */
+int32_t fm_velocity_max_rows(fm_grid grid, fm_env env, int32_t j0, int32_t j1,
+                             double *d_out2, void *stream);
 
 /* Segmented max-abs used by velocity_bound (environment.py:404-419):
  * d_out[s] = max_k |src[(s / inner) * outer_stride + (s % inner) * inner_stride

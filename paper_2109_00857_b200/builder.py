@@ -113,13 +113,25 @@ class DeviceEnv:
         self._vmax = None
         self._vbound = {}
 
-    def velocity_max(self) -> tuple:
-        """Exact max |v_x|, |v_y| over (t, r, cell) -- compute_subgrid's scan."""
+    def velocity_max(self, j_range: tuple | None = None, group=None) -> tuple:
+        """Exact max |v_x|, |v_y| over (t, r, cell) -- compute_subgrid's scan.
+
+        With ``j_range`` (this rank's row strip) and a process ``group``
+        each rank scans its strip and the maxima are combined with one
+        all-reduce (MAX) -- the same value as the full scan."""
         if self._vmax is None:
             torch = _torch()
             out = torch.zeros(2, dtype=torch.float64, device=self.mean.device)
-            _lib.check(_lib.load().fm_velocity_max(self.fm_grid(), self.fm_env(), out.data_ptr(),
-                                                   _lib.stream_ptr()), "fm_velocity_max")
+            if j_range is None:
+                _lib.check(_lib.load().fm_velocity_max(self.fm_grid(), self.fm_env(), out.data_ptr(),
+                                                       _lib.stream_ptr()), "fm_velocity_max")
+            else:
+                _lib.check(_lib.load().fm_velocity_max_rows(self.fm_grid(), self.fm_env(), int(j_range[0]),
+                                                            int(j_range[1]), out.data_ptr(), _lib.stream_ptr()),
+                           "fm_velocity_max_rows")
+                if group is not None or _dist_world() > 1:
+                    import torch.distributed as dist
+                    dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)   # non-negative: max of maxima
             h = out.cpu().numpy()
             self._vmax = (float(h[0]), float(h[1]))
         return self._vmax
@@ -177,6 +189,14 @@ class DeviceEnv:
                 bounds.append(float(per_t.max()))
             self._vbound["b"] = (bounds[0], bounds[1])
         return self._vbound["b"]
+
+
+def _dist_world() -> int:
+    try:
+        import torch.distributed as dist
+        return dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    except Exception:
+        return 1
 
 
 def gate_radius(denv: DeviceEnv, f_max: float) -> tuple:

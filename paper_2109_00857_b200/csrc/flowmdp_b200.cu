@@ -190,7 +190,8 @@ __device__ __forceinline__ float2 ffma2_bcast(float a, float2 b, float2 c)
 static constexpr int kVmaxCells = 2;
 
 template <int NMX>
-__global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_block, const double *cmax, double *out2)
+__global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int cell0, int ncell, int r_per_block,
+                                               const double *cmax, double *out2)
 {
     __shared__ float cs[kVmaxChunk][NMX];
     const int nc = G.nx * G.ny;
@@ -205,9 +206,10 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int r_per_blo
     double delx[kVmaxCells], dely[kVmaxCells];
 #pragma unroll
     for (int q = 0; q < kVmaxCells; ++q) {
-        const int c = blockIdx.x * blockDim.x * kVmaxCells + q * blockDim.x + threadIdx.x;
+        const int lc = blockIdx.x * blockDim.x * kVmaxCells + q * blockDim.x + threadIdx.x;
+        const int c = cell0 + lc;   // cells of the row strip [cell0, cell0 + ncell)
         cell[q] = c;
-        ok[q] = c < nc;
+        ok[q] = lc < ncell;
         mu32[q] = make_float2(0.f, 0.f);
         double Tx = 0.0, Ty = 0.0;
 #pragma unroll
@@ -322,11 +324,17 @@ __global__ void k_maxabs_seg(const double *src, int64_t seg_len, int64_t elem_st
 
 extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *stream)
 {
+    return fm_velocity_max_rows(G, E, 0, G.ny, d_out2, stream);
+}
+
+extern "C" int32_t fm_velocity_max_rows(fm_grid G, fm_env E, int32_t j0, int32_t j1, double *d_out2, void *stream)
+{
     if (G.nx < 1 || G.ny < 1 || G.nt < 1 || E.n_real < 1 || E.n_modes < 0 || E.n_modes > 16)
         return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims (n_modes must be <= 16)");
+    if (j0 < 0 || j1 > G.ny || j0 >= j1) return fm_fail(FM_BAD_ARG, "fm_velocity_max_rows: bad row range");
     cudaStream_t s = (cudaStream_t)stream;
     pool_keep();
-    const int nc = G.nx * G.ny;
+    const int nc = (j1 - j0) * G.nx;   // cells scanned
     const int nm = E.n_modes;
     // max_r |coeff[t, r, m]| per (t, m): the error-bound ingredient
     double *cmax = nullptr;
@@ -346,11 +354,11 @@ extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *st
     }
     dim3 grid(bx, G.nt, (E.n_real + rpb - 1) / rpb);
     if (nm <= 4)
-        k_vmax<4><<<grid, 256, 0, s>>>(G, E, rpb, cmax, d_out2);
+        k_vmax<4><<<grid, 256, 0, s>>>(G, E, j0 * G.nx, nc, rpb, cmax, d_out2);
     else if (nm <= 8)
-        k_vmax<8><<<grid, 256, 0, s>>>(G, E, rpb, cmax, d_out2);
+        k_vmax<8><<<grid, 256, 0, s>>>(G, E, j0 * G.nx, nc, rpb, cmax, d_out2);
     else
-        k_vmax<16><<<grid, 256, 0, s>>>(G, E, rpb, cmax, d_out2);
+        k_vmax<16><<<grid, 256, 0, s>>>(G, E, j0 * G.nx, nc, rpb, cmax, d_out2);
     FM_CK_LAUNCH("k_vmax");
     FM_CK(cudaFreeAsync(cmax, s));
     return FM_OK;

@@ -353,3 +353,21 @@ def test_action_counts_not_dividing_a_warp(heads, speeds):
     for obj in ("time", "net_energy"):
         rcfg = RewardConfig(obj, c_f=1.0, c_r=0.5, r_term=100.0, r_outbound=-300.0)
         _gpu_case(env, acts, rcfg, target)
+
+
+def test_velocity_max_row_strips_combine_to_full_scan():
+    """fm_velocity_max_rows over y-strips, max-combined (what the ranks'
+    all-reduce does), equals the full exact scan bit for bit."""
+    for env in (make_named_env("desk")[0], make_random_env(7009)[0]):
+        de = DeviceEnv.from_host(env)
+        full = de.velocity_max()
+        ny = env.grid.ny
+        cuts = sorted({0, ny // 3, (2 * ny) // 3, ny})
+        parts = []
+        for j0, j1 in zip(cuts[:-1], cuts[1:]):
+            if j0 < j1:
+                de.reset_derived()
+                parts.append(de.velocity_max(j_range=(j0, j1)))
+        comb = (max(p[0] for p in parts), max(p[1] for p in parts))
+        assert np.float64(comb[0]).tobytes() == np.float64(full[0]).tobytes()
+        assert np.float64(comb[1]).tobytes() == np.float64(full[1]).tobytes()
