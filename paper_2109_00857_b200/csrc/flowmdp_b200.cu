@@ -1735,6 +1735,26 @@ static void smem_layout(BuildK &K, int RC, int queue, bool hg = false)
     K.smem_warp = align16(K.off_hg + (hg ? K.CW * K.nslot * (int)sizeof(double) : 0));
 }
 
+// Largest chunk (64 or 32 realizations, >= RW) whose per-warp layout still
+// fits 4 blocks of 4 warps per SM; the smallest if none does.
+static void smem_layout_fit(BuildK &K, int queue, bool hg)
+{
+    static int smem_sm = 0;
+    if (!smem_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess ||
+            smem_sm <= 0)
+            smem_sm = 233472;
+        cudaGetLastError();
+    }
+    const int cands[2] = {K.RW >= FM_BUILD_RC ? K.RW : FM_BUILD_RC, K.RW >= 32 ? K.RW : 32};
+    for (int i = 0; i < 2; ++i) {
+        smem_layout(K, cands[i], queue, hg);
+        if (smem_sm / (4 * K.smem_warp + 1024) >= 4) return;
+    }
+}
+
 template <int FL, int PART>
 static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
 {
@@ -1760,7 +1780,7 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
             // lean net-energy rows read h_cr * g[t+1] from a per-warp slot
             // table (half-size chunks keep 4 blocks per SM)
             BuildK K1 = K;
-            smem_layout(K1, K.RW >= 32 ? K.RW : 32, 0, true);
+            smem_layout_fit(K1, 0, true);
             st = launch_build_p<FL, 1>(K1, (size_t)4 * K1.smem_warp, s);
         } else {
             st = launch_build_p<FL, 1>(K, smem, s);
@@ -1770,7 +1790,7 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
             // obstacle part: per-warp queue of deferred exact segment tests
             // (half-size reconstruction chunks keep it at 4 blocks per SM)
             BuildK K2 = K;
-            smem_layout(K2, K.RW >= 32 ? K.RW : 32, kQueue);
+            smem_layout_fit(K2, kQueue, false);
             return launch_build_p<FL, 2>(K2, (size_t)4 * K2.smem_warp, s);
         } else {
             return launch_build_p<FL, 2>(K, smem, s);
@@ -1956,7 +1976,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.n_tasks = (long long)(h->t1 - h->t0) * K.groups * K.nag;
     if (K.n_tasks > 0xFFFFFFF0LL) return fm_fail(FM_BAD_ARG, "fm_build: too many tasks");
     // realizations per chunk: RW recon lanes per cell, 64 realizations
-    smem_layout(K, K.RW >= FM_BUILD_RC ? K.RW : FM_BUILD_RC, 0);
+    smem_layout_fit(K, 0, false);
     K.src_cell_exact = source_cells_exact(G) ? 1 : 0;
     K.sx_lo = G.nx;
     K.sx_hi = -1;
