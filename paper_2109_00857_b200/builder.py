@@ -132,6 +132,11 @@ class DeviceEnv:
                 if group is not None or _dist_world() > 1:
                     import torch.distributed as dist
                     dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)   # non-negative: max of maxima
+                else:
+                    # a strip's maximum alone is not the field's: never cached
+                    # (the build's proofs rely on the cached value being global)
+                    h = out.cpu().numpy()
+                    return (float(h[0]), float(h[1]))
             h = out.cpu().numpy()
             self._vmax = (float(h[0]), float(h[1]))
         return self._vmax

@@ -371,3 +371,21 @@ def test_velocity_max_row_strips_combine_to_full_scan():
         comb = (max(p[0] for p in parts), max(p[1] for p in parts))
         assert np.float64(comb[0]).tobytes() == np.float64(full[0]).tobytes()
         assert np.float64(comb[1]).tobytes() == np.float64(full[1]).tobytes()
+
+
+@pytest.mark.parametrize("density", [0.04, 0.15])
+def test_dense_random_obstacles(density):
+    """The desk flow (500 realizations, several chunks) with a random static
+    obstacle field: most sources are gated, exact segment tests are frequent
+    (the deferred-test queue overflows and drains in several rounds) and
+    land-masked slots are everywhere; every objective, every block vs the
+    oracle."""
+    from paper_2109_00857_b200 import Environment, ObstacleMask
+    env0, acts, _, target, _ = make_named_env("desk")
+    rng = np.random.default_rng(int(density * 1000))
+    mask = rng.random(env0.obstacles.mask.shape) < density
+    mask[:, target[1], target[0]] = False
+    env = Environment(grid=env0.grid, field=env0.field, scalar=env0.scalar, obstacles=ObstacleMask(mask=mask))
+    for obj in ("time", "energy", "net_energy"):
+        rcfg = RewardConfig(obj, c_f=1.0, c_r=0.5, r_term=100.0, r_outbound=-300.0)
+        _gpu_case(env, acts, rcfg, target)
