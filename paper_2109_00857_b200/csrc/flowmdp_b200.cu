@@ -1184,7 +1184,11 @@ __device__ __forceinline__ void chunk_rows_obst_seq(const BuildK *__restrict__ K
         if (!__all_sync(live, !(rare[0] || rare[1] || rare[2] || rare[3]))) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
+#ifdef FM_EXPERIMENT_NO_SEG
+                if (rare[u]) bad[u] = x1[u] == R.x0;   // timing experiment only: wrong results
+#else
                 if (rare[u]) bad[u] = seg_samples_blocked<FLAGS>(K, t, R.x0, R.y0, x1[u], y1[u]);
+#endif
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
