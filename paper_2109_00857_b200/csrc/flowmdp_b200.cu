@@ -947,11 +947,26 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
     if ((FLAGS & F_CNT) && nk == FM_BUILD_RC) {
         // full chunk: the batch loop unrolled (no loop-carried branch; the
         // scheduler may interleave consecutive batches)
+#ifndef FM_LEAN_NO_PREFETCH
+        // velocities of the next batch loaded before this batch's math
+        double2 vn[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) vn[u] = vrow[u];
+#endif
 #pragma unroll
         for (int kb = 0; kb < FM_BUILD_RC; kb += U) {
             double2 v[U];
+#ifndef FM_LEAN_NO_PREFETCH
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = vn[u];
+            if (kb + U < FM_BUILD_RC) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) vn[u] = vrow[kb + U + u];
+            }
+#else
 #pragma unroll
             for (int u = 0; u < U; ++u) v[u] = vrow[kb + u];
+#endif
             int q[U];
             double w[U];
 #pragma unroll
