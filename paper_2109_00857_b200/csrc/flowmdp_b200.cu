@@ -910,14 +910,10 @@ __device__ __forceinline__ void hist_inc(uint16_t *h16q, unsigned hs_word, int q
 {
 #ifdef FM_HIST_ATOMS
     (void)h16q;
-#ifdef FM_RED_CLOBBER
-    asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(hs_word + (unsigned)q * 64u), "r"(half_one) : "memory");
-#else
     // no memory clobber: the velocity loads of the next batch may be hoisted
     // above these reductions (they never alias the histogram); the callers
     // fence the compiler before the histogram is read with plain loads
     asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(hs_word + (unsigned)q * 64u), "r"(half_one));
-#endif
 #else
     (void)hs_word;
     h16q[q * 32] += (uint16_t)((half_one & 0xFFFFu) | (half_one >> 16));   // the increment, whichever half
@@ -981,9 +977,6 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
         return;
     }
 #endif
-#ifdef FM_LEAN_UNROLL2
-#pragma unroll 2
-#endif
     for (; k + U <= nk; k += U) {
         double2 v[U];
 #pragma unroll
@@ -996,21 +989,8 @@ __device__ __forceinline__ void chunk_rows_lean(const BuildK &K, const RowC &R, 
 #pragma unroll
             for (int u = 0; u < U; ++u) S = DADD(S, w[u]);
         }
-#if defined(FM_HIST_PAIR) && !defined(FM_HIST_ATOMS)
-        // two counters per step: both loads issue before either store, so the
-        // read-modify-write chain is half as long; equal slots add 2 (the
-        // second store, which lands last, carries the sum)
-#pragma unroll
-        for (int u = 0; u < U; u += 2) {
-            uint16_t *pa = h16q + q[u] * 32, *pb = h16q + q[u + 1] * 32;
-            const unsigned ca = *pa, cb = *pb;
-            *pa = (uint16_t)(ca + 1u);
-            *pb = (uint16_t)(cb + 1u + (q[u] == q[u + 1] ? 1u : 0u));
-        }
-#else
 #pragma unroll
         for (int u = 0; u < U; ++u) hist_inc(h16q, hs_word, q[u], half_one);
-#endif
     }
     for (; k < nk; ++k) {
         double w0;
@@ -1089,7 +1069,6 @@ __device__ __forceinline__ void chunk_rows_obst_cnt(const BuildK *__restrict__ K
         if (r0) pend |= 1ull << (k & 63);
         else hist_inc(h16q, hs_word, q0, half_one);
     }
-#ifndef FM_EXPERIMENT_NO_RARE   // timing experiment only: wrong results
     // drain: the live lanes park their deferred transitions in the warp's
     // queue, then every lane of the warp takes queue entries round-robin
     // (the exact tests of one busy row are spread over all 32 lanes)
@@ -1133,11 +1112,7 @@ __device__ __forceinline__ void chunk_rows_obst_cnt(const BuildK *__restrict__ K
             const int c = K.cell0 + grp * K.CW + owner / K.AG;
             const double x0 = DADD(K.ox, DMUL(DADD((double)(c % K.nx), 0.5), K.dx));   // environment.py:99-100
             const double y0 = DADD(K.oy, DMUL(DADD((double)(c / K.nx), 0.5), K.dx));
-#ifdef FM_EXPERIMENT_NO_SEG   // timing experiment only: wrong results
-            const int sl = (x0 == it.x1 && y0 == it.y1) ? K.nslot : slot;
-#else
             const int sl = seg_samples_blocked<FLAGS>(K, t, x0, y0, it.x1, it.y1) ? K.nslot : slot;
-#endif
             // the owner's u16 counter [slot][owner] lives in word (slot * 16 + owner / 2)
             asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(hist_s + (unsigned)sl * 64u + (unsigned)(owner >> 1) * 4u),
                          "r"(1u << ((owner & 1) * 16))
@@ -1145,7 +1120,6 @@ __device__ __forceinline__ void chunk_rows_obst_cnt(const BuildK *__restrict__ K
         }
         __syncwarp();
     }
-#endif
 }
 
 // Obstacle-warp realization loop under F_PROVEN without F_CNT (net_energy,
@@ -1199,11 +1173,7 @@ __device__ __forceinline__ void chunk_rows_obst_seq(const BuildK *__restrict__ K
         if (!__all_sync(live, !(rare[0] || rare[1] || rare[2] || rare[3]))) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-#ifdef FM_EXPERIMENT_NO_SEG
-                if (rare[u]) bad[u] = x1[u] == R.x0;   // timing experiment only: wrong results
-#else
                 if (rare[u]) bad[u] = seg_samples_blocked<FLAGS>(K, t, R.x0, R.y0, x1[u], y1[u]);
-#endif
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
