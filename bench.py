@@ -239,13 +239,15 @@ def run_ours(args):
             device_solve_sharded(dm, values, policy, j0, j1)
         else:
             solve_backward(dm, values, policy)
+        s1 = ev()
+        s1.record()
         if dm.check():                           # capacity miss: rebuilt, solve again
             if world > 1:
                 values.zero_()
                 device_solve_sharded(dm, values, policy, j0, j1)
             else:
                 solve_backward(dm, values, policy)
-        build_ev.append((b0, b1, dm.nnz))
+        build_ev.append((b0, b1, dm.nnz, s1))
         return dm
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
@@ -275,7 +277,8 @@ def run_ours(args):
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = w.transitions / (ms_per_step / 1e3)
-    build_ms = statistics.median(b0.elapsed_time(b1) for b0, b1, _ in build_ev)
+    build_ms = statistics.median(e[0].elapsed_time(e[1]) for e in build_ev)
+    solve_ms = statistics.median(e[1].elapsed_time(e[3]) for e in build_ev)
 
     # ---- end to end through the public API, pinned host buffers --------------
     pinned = {
@@ -347,6 +350,26 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # backward solve against HBM: 12 B per entry (4 B column
+    # + 8 B probability), 8 B reward per (state, action) row, 18 B per state
+    # (V_{t+1} read, V_t write, policy) -- the reference's COO layout; the
+    # compact model moves 4 B per entry, so the algorithmic figure is an
+    # upper bound on the bytes this kernel needs
+    n_rows_rank = (j1 - j0) * g.nx * g.nt * w.n_actions
+    solve_bytes = 12 * build_ev[-1][2] + 8 * n_rows_rank + 18 * (j1 - j0) * g.nx * g.nt
+    hbm_peak, hbm_src = 6650.0, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        try:
+            pk = json.load(open(mp))
+            for key in ("hbm_gbps", "hbm_GBps", "hbm_copy_gbps", "hbm_burst_gbps"):
+                if key in pk:
+                    hbm_peak, hbm_src = float(pk[key]), f"MEASURED_PEAKS.json:{key}"
+                    break
+        except Exception:
+            pass
+    solve_gbps = solve_bytes / (solve_ms / 1e3) / 1e9
+
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -360,7 +383,8 @@ def run_ours(args):
                        "realizations": w.n_realizations, "modes": w.n_modes, "objective": w.objective,
                        "transitions": w.transitions, "parallelism": f"ystrips{world}",
                        "l2": "flushed between steps (256 MiB write); inputs 185 MB > L2"},
-            "stages": {"build_ms_median": build_ms, "step_ms": ms_per_step, "nnz": build_ev[-1][2]},
+            "stages": {"build_ms_median": build_ms, "solve_ms_median": solve_ms, "step_ms": ms_per_step,
+                       "nnz": build_ev[-1][2]},
             "e2e": {"value": e2e_value, "unit": "transitions/s", "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h * world, "ms_per_step": e2e_ms / args.steps},
             "roofline": {"bound": "fp64", "kernel": "k_build", "achieved": achieved / 1e12, "peak": peak / 1e12,
@@ -372,6 +396,10 @@ def run_ours(args):
                                        "fewer (identity ops skipped, floor as one DADD, count-formed rewards: "
                                        "6 + 32/|A| FP64 per transition), see the ncu pipe figures",
                          **pipe},
+            "solve_roofline": {"bound": "hbm", "kernel": "k_solve_layer (backward sweep, nt launches)",
+                               "achieved": solve_gbps, "peak": hbm_peak, "unit": "GB/s", "frac": solve_gbps / hbm_peak,
+                               "bytes_algorithmic": solve_bytes, "ms": solve_ms, "peak_source": hbm_src,
+                               "note": "nt dependent layers: latency-bound, not bandwidth-bound"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
