@@ -1377,7 +1377,11 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
             // realization -> SINK with r_outbound, then the dead override.
             if (row_ok) {
                 const double rw = terminal ? 0.0 : K.r_out;
-                for (int r = 0; r < nr; ++r) S = DADD(S, rw);
+                if (FLAGS & F_CNT) {
+                    S = DADD(DMUL((double)nr, rw), 0.0);   // exact under F_CNT: the loop's sum
+                } else {
+                    for (int r = 0; r < nr; ++r) S = DADD(S, rw);
+                }
                 h16[nslot * 32] = (uint16_t)nr;
             }
         } else {
