@@ -1751,13 +1751,31 @@ static void smem_layout_fit(BuildK &K, int queue, bool hg)
 template <int FL, int PART>
 static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
 {
+    (void)smem;   // recomputed: 4 warps per block, fewer when a warp's layout is large
     auto kern = k_build<FL, PART>;
-    FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static int max_block = 0;
+    if (!max_block) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&max_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+            max_block <= 0)
+            max_block = 232448;
+        cudaGetLastError();
+    }
+    int wpb = max_block / K.smem_warp;
+    if (wpb > 4) wpb = 4;
+    if (wpb < 1)
+        return fm_fail(FM_BAD_ARG,
+                       "sub-grid of %d slots needs %d B of shared memory per warp (at most %d per block on this "
+                       "device)",
+                       K.nslot + 1, K.smem_warp, max_block);
+    const size_t bytes = (size_t)wpb * K.smem_warp;
+    FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     int occ = 0;
-    FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));
-    if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", smem);
+    FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * wpb, bytes));
+    if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", bytes);
     FM_CK(cudaMemsetAsync(K.task_counter, 0, sizeof(unsigned int), s));
-    kern<<<occ * sm_count(), 128, smem, s>>>(K);
+    kern<<<occ * sm_count(), 32 * wpb, bytes, s>>>(K);
     FM_CK_LAUNCH("k_build");
     return FM_OK;
 }
