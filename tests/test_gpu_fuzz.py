@@ -114,3 +114,46 @@ def test_fuzz_shrunk_subgrid(seed):
         with pytest.raises(fm.ContractViolation) as ei:
             fm.build_model(ctx, sub)
         assert str(ei.value) == ref_err
+
+
+def _edge_world(nx, ny, nt, nr, nm, n_h, n_s, mask_all_t1=False, seed=1):
+    rng = np.random.default_rng(seed)
+    g = GridSpec(nx=nx, ny=ny, nt=nt, dx=1.0, dt=1.0)
+    mask = np.zeros((nt, ny, nx), dtype=bool)
+    if mask_all_t1 and nt > 1:
+        mask[1] = True
+        mask[1, 0, 0] = False
+    env = Environment(grid=g,
+                      field=DOVelocityField(mean=rng.normal(0, 0.5, (nt, ny, nx, 2)),
+                                            modes=rng.normal(0, 0.3, (nm, nt, ny, nx, 2)),
+                                            coeffs=rng.normal(0, 0.5, (nt, nr, nm))),
+                      scalar=ScalarMeanField(g_mean=rng.uniform(0, 2, (nt, ny, nx))),
+                      obstacles=ObstacleMask(mask=mask))
+    return env, ActionSpace(n_headings=n_h, n_speeds=n_s, f_max=1.0)
+
+
+@pytest.mark.parametrize("case", [
+    dict(nx=5, ny=4, nt=1, nr=7, nm=2, n_h=4, n_s=1),          # horizon layer only
+    dict(nx=5, ny=4, nt=2, nr=1, nm=1, n_h=4, n_s=2),          # one realization
+    dict(nx=1, ny=7, nt=4, nr=70, nm=3, n_h=4, n_s=1),         # one column
+    dict(nx=9, ny=1, nt=4, nr=70, nm=0, n_h=8, n_s=1),         # one row, no modes
+    dict(nx=6, ny=6, nt=4, nr=65, nm=8, n_h=1, n_s=1),         # a single action
+    dict(nx=6, ny=6, nt=5, nr=64, nm=8, n_h=16, n_s=2, mask_all_t1=True),   # 32 actions, layer 1 all masked
+    dict(nx=7, ny=5, nt=3, nr=129, nm=5, n_h=5, n_s=3),        # 15 actions, 3 chunks + 1
+])
+def test_edge_shapes(case):
+    env, acts = _edge_world(**case)
+    for obj, target in (("time", (0, 0)), ("net_energy", (env.grid.nx - 1, env.grid.ny - 1))):
+        rcfg = RewardConfig(obj, c_f=1.0, c_r=0.5, r_term=10.0, r_outbound=-30.0)
+        ctx = StepContext(env, acts, rcfg, target)
+        sub = fm.compute_subgrid(env.field, acts, env.grid)
+        hx, hy = O.compute_subgrid(env.field, acts.f_max, env.grid)
+        assert (sub.half_width_x, sub.half_width_y) == (hx, hy)
+        om = O.build_model(env, acts, rcfg, target, hx, hy)
+        assert model_digest(fm.build_model(ctx, sub)) == model_digest(om)
+        dmc = build_device_model(ctx.device_env(), acts, rcfg, target, sub, lean=False)
+        assert model_digest(dmc.to_sparse_model()) == model_digest(om)
+        ov, oa, oit, ores, oconv = O.value_iteration(om)
+        pv = fm.value_iteration(fm.build_model(ctx, sub))
+        assert sha(pv.values) == sha(ov) and sha(pv.actions) == sha(oa)
+        assert (pv.iterations_run, pv.residual, pv.converged) == (oit, ores, oconv)
