@@ -43,6 +43,9 @@ def _args():
     p.add_argument("--workload", default=WORKLOAD)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo: validation of the N>1 path with several ranks on one GPU (halo and maxima "
+                        "staged through host memory); never a bench number")
     return p.parse_args()
 
 
@@ -191,15 +194,20 @@ def run_ours(args):
     import paper_2109_00857_b200 as fm
     from paper_2109_00857_b200 import _lib, workloads
     from paper_2109_00857_b200.builder import DeviceEnv, build_device_model, subgrid_from_vmax
-    from paper_2109_00857_b200.sharding import device_solve_sharded, strip_bounds
+    from paper_2109_00857_b200.sharding import all_reduce_max, device_solve_sharded, strip_bounds
     from paper_2109_00857_b200.solver import solve_backward
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":   # ranks may share a GPU
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     L = _lib.load()
     s = _lib.stream_ptr()
 
@@ -273,7 +281,7 @@ def run_ours(args):
     total_ms = sum(times)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_max(t)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = w.transitions / (ms_per_step / 1e3)
@@ -326,7 +334,7 @@ def run_ours(args):
     e2e_ms = sum(e2e_times)
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_max(t)
         e2e_ms = float(t.item())
     e2e_value = w.transitions / (e2e_ms / args.steps / 1e3)
 
@@ -381,7 +389,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "grid": [g.nx, g.ny, g.nt], "actions": w.n_actions,
                        "realizations": w.n_realizations, "modes": w.n_modes, "objective": w.objective,
-                       "transitions": w.transitions, "parallelism": f"ystrips{world}",
+                       "transitions": w.transitions, "parallelism": f"ystrips{world}" + ("-gloo-validation" if args.dist_backend == "gloo" else ""),
                        "l2": "flushed between steps (256 MiB write); inputs 185 MB > L2"},
             "stages": {"build_ms_median": build_ms, "solve_ms_median": solve_ms, "step_ms": ms_per_step,
                        "nnz": build_ev[-1][2]},

@@ -130,8 +130,8 @@ class DeviceEnv:
                                                             int(j_range[1]), out.data_ptr(), _lib.stream_ptr()),
                            "fm_velocity_max_rows")
                 if group is not None or _dist_world() > 1:
-                    import torch.distributed as dist
-                    dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)   # non-negative: max of maxima
+                    from .sharding import all_reduce_max
+                    all_reduce_max(out, group)   # non-negative: max of maxima
                 else:
                     # a strip's maximum alone is not the field's: never cached
                     # (the build's proofs rely on the cached value being global)

@@ -44,6 +44,29 @@ def halo_plan(ny: int, world: int, rank: int, hy: int) -> tuple:
     return sends, recvs
 
 
+def host_staged(tensor, group=None) -> bool:
+    """True when ``tensor`` lives on a GPU but the group's backend moves host
+    memory only (gloo): the exchange then stages through host buffers.  This
+    is the test configuration that runs several ranks on one GPU (NCCL
+    refuses two ranks on one device); production runs NCCL on device
+    buffers."""
+    import torch.distributed as dist
+
+    return tensor.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def all_reduce_max(tensor, group=None) -> None:
+    """In-place MAX all-reduce (device buffers under NCCL)."""
+    import torch.distributed as dist
+
+    if host_staged(tensor, group):
+        h = tensor.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        tensor.copy_(h)
+    else:
+        dist.all_reduce(tensor, op=dist.ReduceOp.MAX, group=group)
+
+
 def exchange_layer(values, t: int, nx: int, ny: int, hy: int, group=None) -> int:
     """Exchange halo rows of layer t of the flat value vector in place.
     Returns the number of bytes this rank sent."""
@@ -55,17 +78,26 @@ def exchange_layer(values, t: int, nx: int, ny: int, hy: int, group=None) -> int
         return 0
     sends, recvs = halo_plan(ny, world, rank, hy)
     base = t * nx * ny
-    ops = []
+    staged = host_staged(values, group)
+    ops, landing = [], []
     sent = 0
     for peer, r0, r1 in sends:
         buf = values[base + r0 * nx: base + r1 * nx]
+        if staged:
+            buf = buf.cpu()
         ops.append(dist.P2POp(dist.isend, buf, peer, group))
         sent += buf.numel() * buf.element_size()
     for peer, r0, r1 in recvs:
-        ops.append(dist.P2POp(dist.irecv, values[base + r0 * nx: base + r1 * nx], peer, group))
+        dst = values[base + r0 * nx: base + r1 * nx]
+        buf = dst.new_empty(dst.shape, device="cpu") if staged else dst
+        if staged:
+            landing.append((dst, buf))
+        ops.append(dist.P2POp(dist.irecv, buf, peer, group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    for dst, buf in landing:
+        dst.copy_(buf)
     return sent
 
 

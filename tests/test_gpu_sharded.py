@@ -1,0 +1,108 @@
+"""The N>1 planner path on real kernels: y-strip builds (k_build), strip
+velocity scans + MAX all-reduce (k_vmax), and the strip backward solve
+(k_solve_layer) with per-layer halo exchange (sharding.py).
+
+The pool gives one GPU per run and NCCL refuses two ranks on one device, so
+the ranks share cuda:0 over gloo (halo and maxima staged through host
+memory); everything below the exchange is the production code.  The union
+of the strips must equal the oracle's Jacobi values / greedy actions bit for
+bit, and every rank must size the same sub-grid as the full scan."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import make_named_env, make_random_env
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, case, out_path):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2109_00857_b200.builder import DeviceEnv, build_device_model, subgrid_from_vmax
+    from paper_2109_00857_b200.sharding import device_solve_sharded, strip_bounds
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    env, acts, rcfg, target = case()
+    g = env.grid
+    j0, j1 = strip_bounds(g.ny, world, rank)
+    de = DeviceEnv.from_host(env)
+    vm = de.velocity_max(j_range=(j0, j1))        # strip scan + all-reduce
+    sub = subgrid_from_vmax(vm, acts.f_max, g)
+    dm = build_device_model(de, acts, rcfg, target, sub, j_range=(j0, j1))
+    values = torch.zeros(g.n_states + 1, dtype=torch.float64, device="cuda")
+    policy = torch.zeros(g.n_states, dtype=torch.int16, device="cuda")
+    device_solve_sharded(dm, values, policy, j0, j1)
+    v, p = values.cpu().numpy(), policy.cpu().numpy().view(np.uint16)
+    mine_v, mine_p = np.zeros(g.n_states + 1), np.zeros(g.n_states, dtype=np.uint16)
+    for t in range(g.nt):
+        a, b = t * g.n_cells + j0 * g.nx, t * g.n_cells + j1 * g.nx
+        mine_v[a:b], mine_p[a:b] = v[a:b], p[a:b]
+    np.save(f"{out_path}.{rank}.v.npy", mine_v)
+    np.save(f"{out_path}.{rank}.p.npy", mine_p)
+    np.save(f"{out_path}.{rank}.sub.npy", np.array([sub.half_width_x, sub.half_width_y]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _case_random():
+    return make_random_env(7004)
+
+
+def _case_random_obst():
+    return make_random_env(7011)
+
+
+def _case_smoke():
+    env, acts, rcfg, target, _ = make_named_env("smoke")
+    return env, acts, rcfg, target
+
+
+def _case_desk():
+    env, acts, rcfg, target, _ = make_named_env("desk")
+    return env, acts, rcfg, target
+
+
+@pytest.mark.parametrize("case,world", [(_case_random, 2), (_case_random_obst, 3), (_case_smoke, 2),
+                                        (_case_smoke, 3), (_case_desk, 2), (_case_desk, 4)])
+def test_sharded_planner_on_device(tmp_path, case, world):
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "s")
+    mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
+    env, acts, rcfg, target = case()
+    hx, hy = O.compute_subgrid(env.field, acts.f_max, env.grid)
+    for r in range(world):
+        assert tuple(np.load(f"{out}.{r}.sub.npy")) == (hx, hy)
+    full = O.build_model(env, acts, rcfg, target, hx, hy, n_threads=os.cpu_count() or 1)
+    ref_v, ref_a, _, res, _ = O.value_iteration(full)
+    g = env.grid
+    got_v, got_p = np.zeros(g.n_states + 1), np.zeros(g.n_states, dtype=np.uint16)
+    from paper_2109_00857_b200.sharding import strip_bounds
+    for r in range(world):   # assemble by copying (a sum would turn -0.0 into +0.0)
+        v, p = np.load(f"{out}.{r}.v.npy"), np.load(f"{out}.{r}.p.npy")
+        j0, j1 = strip_bounds(g.ny, world, r)
+        for t in range(g.nt):
+            a, b = t * g.n_cells + j0 * g.nx, t * g.n_cells + j1 * g.nx
+            got_v[a:b], got_p[a:b] = v[a:b], p[a:b]
+    assert res == 0.0   # finite horizon: Jacobi converges exactly, so the backward sweep must equal it
+    assert got_v.tobytes() == ref_v.tobytes()
+    assert np.array_equal(got_p, ref_a.astype(np.uint16))
