@@ -442,7 +442,12 @@ extern "C" int32_t fm_mask_sat(const uint8_t *mask, int32_t nt, int32_t ny, int3
 //   fits in 2^30 -> lean rows need no window test and floor by magic add.
 // F_CNT: the host proved every reward value dyadic with an exact sequential
 //   sum -> lean rows form the reward sum from the histogram counts.
-enum : int { F_DT_ONE = 1, F_OX_ZERO = 2, F_DX_MUL = 4, F_DX_ONE = 8, F_NET = 16, F_PROVEN = 32, F_CNT = 64 };
+// F_GHIST: the sub-grid's per-warp histogram does not fit in shared memory
+//   -> it lives in a global scratch slice per resident warp (same [slot][lane]
+//   u16 layout, coalesced), fully checked rows only.
+enum : int {
+    F_DT_ONE = 1, F_OX_ZERO = 2, F_DX_MUL = 4, F_DX_ONE = 8, F_NET = 16, F_PROVEN = 32, F_CNT = 64, F_GHIST = 128
+};
 enum : int { RF_DEAD = 1, RF_TERMINAL = 2, RF_GATE = 4, RF_LANDWIN = 8, RF_SEGWIN = 16 };
 
 struct BuildK {
@@ -484,6 +489,7 @@ struct BuildK {
     unsigned long long *nnz_counter;
     uint32_t *viol;
     unsigned int *task_counter;
+    uint16_t *ghist;   // F_GHIST: [resident warp][nslot + 1][32]
 };
 
 // fl(q / n) for 0 <= q <= n <= kFracMaxN at g_frac[n (n + 1) / 2 + q]: the
@@ -1274,7 +1280,9 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *wbase = smem + (size_t)warp * K.smem_warp;
-    uint16_t *hist16 = reinterpret_cast<uint16_t *>(wbase);                 // [nslot+1][32]
+    uint16_t *hist16 = (FLAGS & F_GHIST)                                     // [nslot+1][32]
+                           ? K.ghist + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * (size_t)(K.nslot + 1) * 32
+                           : reinterpret_cast<uint16_t *>(wbase);
     uint16_t *h16 = hist16 + lane;
     double2 *vbuf = reinterpret_cast<double2 *>(wbase + K.off_vbuf);       // [CW][RC+1]
     double *coefT = reinterpret_cast<double *>(wbase + K.off_coef);        // [nm][RC]
@@ -1713,13 +1721,26 @@ __global__ void k_viol_report(const __grid_constant__ BuildK K, int t, int a, in
 
 static int align16(int x) { return (x + 15) & ~15; }
 
+static int smem_block_optin()
+{
+    static int v = 0;
+    if (!v) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || v <= 0)
+            v = 232448;
+        cudaGetLastError();
+    }
+    return v;
+}
+
 // Per-warp shared memory: u16 histogram [nslot+1][32] | v chunk [CW][RC+1]
 // | transposed coefficients [nm][RC] | modes [CW][nm] | danger classes
 // [CW][2 words per 32 slots] | (queue entries) deferred exact tests.
-static void smem_layout(BuildK &K, int RC, int queue, bool hg = false)
+static void smem_layout(BuildK &K, int RC, int queue, bool hg = false, bool ghist = false)
 {
     K.RC = RC;
-    K.off_vbuf = align16((K.nslot + 1) * 64);
+    K.off_vbuf = ghist ? 0 : align16((K.nslot + 1) * 64);
     K.off_coef = K.off_vbuf + K.CW * (K.RC + 1) * (int)sizeof(double2);
     K.off_modes = align16(K.off_coef + K.RC * K.nm * (int)sizeof(double));
     K.off_danger = align16(K.off_modes + K.CW * K.nm * (int)sizeof(double2));
@@ -1809,8 +1830,46 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
     }
 }
 
+// Sub-grids whose histogram exceeds a block's shared memory: the checked
+// kernel with the histogram in a stream-ordered global scratch buffer, one
+// slice per warp of a persistent grid (tasks come from the task counter, so
+// any grid size covers them; the grid shrinks to keep the scratch <= 4 GiB).
+template <int FL>
+static int32_t launch_build_ghist(BuildK K, cudaStream_t s)
+{
+    auto kern = k_build<FL, 0>;
+    int max_block = 0, dev = 0;
+    FM_CK(cudaGetDevice(&dev));
+    FM_CK(cudaDeviceGetAttribute(&max_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    int wpb = max_block / K.smem_warp;
+    if (wpb > 4) wpb = 4;
+    if (wpb < 1)
+        return fm_fail(FM_BAD_ARG, "sub-grid of %d slots: %d B of per-warp state exceed a block's shared memory",
+                       K.nslot + 1, K.smem_warp);
+    const size_t bytes = (size_t)wpb * K.smem_warp;
+    FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    int occ = 0;
+    FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * wpb, bytes));
+    if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", bytes);
+    const size_t per_block = (size_t)wpb * (size_t)(K.nslot + 1) * 64;
+    long long blocks = (long long)occ * sm_count();
+    const long long cap = (long long)((4ull << 30) / per_block);
+    if (blocks > cap) blocks = cap > 0 ? cap : 1;
+    FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&K.ghist), (size_t)blocks * per_block, s));
+    FM_CK(cudaMemsetAsync(K.task_counter, 0, sizeof(unsigned int), s));
+    kern<<<(unsigned)blocks, 32 * wpb, bytes, s>>>(K);
+    FM_CK_LAUNCH("k_build");
+    FM_CK(cudaFreeAsync(K.ghist, s));
+    return FM_OK;
+}
+
 static int32_t launch_build(const BuildK &K, int flags, size_t smem, cudaStream_t s)
 {
+    if (flags & F_GHIST) {
+        // identity geometry flags dropped: x*1, x/1, x-0 are exact
+        if (flags & F_NET) return launch_build_ghist<F_GHIST | F_NET>(K, s);
+        return launch_build_ghist<F_GHIST>(K, s);
+    }
     if (flags & F_PROVEN) {
         // lean variants exist for the identity geometry (dt = dx = 1, origin
         // 0) and the general one; dropping identity flags never changes a
@@ -2021,6 +2080,11 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
         sterbenz_axis(G.nx, G.ox, G.dx, Rx, K.sx_lo, K.sx_hi);
         sterbenz_axis(G.ny, G.oy, G.dx, Ry, K.sy_lo, K.sy_hi);
         if (K.obj != FM_OBJ_NET_ENERGY && rewards_sum_exactly(h)) flags |= F_CNT;
+    }
+    if (K.smem_warp > smem_block_optin()) {
+        // the shared histogram does not fit even one warp: global fallback
+        smem_layout(K, K.RW >= 32 ? K.RW : 32, 0, false, true);
+        flags = (flags & F_NET) | F_GHIST;
     }
     return FM_OK;
 }

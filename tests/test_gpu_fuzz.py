@@ -157,3 +157,36 @@ def test_edge_shapes(case):
         pv = fm.value_iteration(fm.build_model(ctx, sub))
         assert sha(pv.values) == sha(ov) and sha(pv.actions) == sha(oa)
         assert (pv.iterations_run, pv.residual, pv.converged) == (oit, ores, oconv)
+
+
+@pytest.mark.parametrize("objective", ["time", "net_energy"])
+def test_huge_subgrid_global_histogram(objective):
+    """A sub-grid whose per-warp histogram (64 B per slot) exceeds a block's
+    shared memory: the build takes the global-histogram kernel (F_GHIST) and
+    still matches the reference bit for bit."""
+    rng = np.random.default_rng(77)
+    nx = ny = 72
+    nt, nr, nm = 3, 40, 3
+    g = GridSpec(nx=nx, ny=ny, nt=nt, dx=1.0, dt=1.0)
+    mask = np.zeros((nt, ny, nx), dtype=bool)
+    mask[:, 30:34, 20:26] = True
+    env = Environment(grid=g,
+                      field=DOVelocityField(mean=rng.uniform(-30.0, 30.0, (nt, ny, nx, 2)),
+                                            modes=rng.normal(0, 0.4, (nm, nt, ny, nx, 2)),
+                                            coeffs=rng.normal(0, 0.5, (nt, nr, nm))),
+                      scalar=ScalarMeanField(g_mean=rng.uniform(0, 2, (nt, ny, nx))),
+                      obstacles=ObstacleMask(mask=mask))
+    acts = ActionSpace(n_headings=8, n_speeds=1, f_max=1.0)
+    rcfg = RewardConfig(objective, c_f=1.0, c_r=0.5, r_term=10.0, r_outbound=-30.0)
+    target = (40, 40)
+    hx, hy = O.compute_subgrid(env.field, acts.f_max, env.grid)
+    assert ((2 * hx + 1) * (2 * hy + 1) + 1) * 64 > 232448   # beyond shared memory
+    ctx = StepContext(env, acts, rcfg, target)
+    sub = fm.compute_subgrid(env.field, acts, env.grid)
+    assert (sub.half_width_x, sub.half_width_y) == (hx, hy)
+    om = O.build_model(env, acts, rcfg, target, hx, hy, n_threads=os.cpu_count() or 1)
+    assert model_digest(fm.build_model(ctx, sub)) == model_digest(om)
+    ov, oa, oit, ores, oconv = O.value_iteration(om)
+    assert ores == 0.0
+    vals, pol = solve_backward(build_device_model(ctx.device_env(), acts, rcfg, target, sub))
+    assert sha(vals.cpu().numpy()) == sha(ov)
