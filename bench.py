@@ -230,8 +230,9 @@ def run_ours(args):
     build_ev = []
     prev = {}
 
-    def step(de):
-        de.reset_derived()                       # sub-grid and gate statistics are recomputed every step
+    def step(de, scanned=False):
+        if not scanned:
+            de.reset_derived()                   # sub-grid and gate statistics are recomputed every step
         # k_vmax over this rank's strip (+ a MAX all-reduce across ranks):
         # the one host round trip before the build
         vm = de.velocity_max(j_range=(j0, j1)) if world > 1 else de.velocity_max()
@@ -314,8 +315,10 @@ def run_ours(args):
         torch.cuda.synchronize()
         e0, e1 = ev(), ev()
         e0.record()
-        de = DeviceEnv.from_host(_HostEnv, non_blocking=True)
-        step(de)
+        # upload in time slabs, the exact sub-grid scan of each slab overlapping
+        # the next slab's copy (the planner's host-input path)
+        de = DeviceEnv.from_host_scanned(_HostEnv, j_range=(j0, j1) if world > 1 else None)
+        step(de, scanned=True)
         if world == 1:
             host_v.copy_(values, non_blocking=True)
             host_p.copy_(policy, non_blocking=True)

@@ -148,6 +148,11 @@ int32_t fm_velocity_max(fm_grid grid, fm_env env, double *d_out2, void *stream);
  * global maximum is the max over strips, e.g. an all-reduce). */
 int32_t fm_velocity_max_rows(fm_grid grid, fm_env env, int32_t j0, int32_t j1,
                              double *d_out2, void *stream);
+/* The scan over layers [t0, t1) x rows [j0, j1), max-accumulated into d_out2:
+ * lets a caller scan each time slab as its host->device copy lands (the
+ * maxima over slabs are the full scan's). */
+int32_t fm_velocity_max_slab(fm_grid grid, fm_env env, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
+                             double *d_out2, void *stream);
 
 /* Segmented max-abs used by velocity_bound (environment.py:404-419):
  * d_out[s] = max_k |src[(s / inner) * outer_stride + (s % inner) * inner_stride

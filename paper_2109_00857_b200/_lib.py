@@ -122,6 +122,8 @@ SIGNATURES = {
     "fm_kernel_launches": (C.c_int64, []),
     "fm_velocity_max": (C.c_int32, [FmGrid, FmEnv, C.c_void_p, C.c_void_p]),
     "fm_velocity_max_rows": (C.c_int32, [FmGrid, FmEnv, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "fm_velocity_max_slab": (C.c_int32, [FmGrid, FmEnv, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                         C.c_void_p]),
     "fm_maxabs_segments": (C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                        C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
     "fm_mask_sat": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),

@@ -52,6 +52,7 @@ class DeviceEnv:
     _vbound: dict = field(default_factory=dict)
     _vmax: tuple | None = None
     _acts: dict = field(default_factory=dict)
+    _scan: tuple | None = None   # (device maxima, j_range) of a scan done during upload
 
     def action_table(self, recs: np.ndarray):
         """Device copy of an action-record table (cached by content)."""
@@ -91,6 +92,64 @@ class DeviceEnv:
         de._make_sat()
         return de
 
+    @classmethod
+    def from_host_scanned(cls, env, slabs: int = 8, j_range: tuple | None = None, device=None):
+        """Upload in time slabs on a copy stream and run compute_subgrid's
+        exact scan (fm_velocity_max_slab) on each slab as soon as it lands,
+        so the scan overlaps the rest of the host->device transfer.  The
+        maxima stay on the device until ``velocity_max`` reads them (with
+        ``j_range``: this rank's strip only, combined there by all-reduce).
+        Inputs: numpy arrays or CPU torch tensors (pinned for a real overlap)."""
+        torch = _torch()
+        _lib.load()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        grid, fld = env.grid, env.field
+
+        def host(a):
+            return a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+
+        mask_src = env.obstacles.mask
+        if isinstance(mask_src, np.ndarray):
+            mask_src = mask_src.view(np.uint8) if mask_src.dtype == np.bool_ else mask_src.astype(np.uint8)
+        src = {"mean": host(fld.mean), "modes": host(fld.modes), "coeffs": host(fld.coeffs),
+               "g": host(env.scalar.g_mean), "mask": host(mask_src)}
+        dt = {"mean": torch.float64, "modes": torch.float64, "coeffs": torch.float64, "g": torch.float64,
+              "mask": torch.uint8}
+        for k, v in src.items():
+            if v.dtype != dt[k] or not v.is_contiguous():
+                src[k] = v.to(dt[k]).contiguous()
+        dst = {k: torch.empty(v.shape, dtype=dt[k], device=dev) for k, v in src.items()}
+        de = cls(grid=grid, mean=dst["mean"], modes=dst["modes"], coeffs=dst["coeffs"], g=dst["g"],
+                 mask=dst["mask"], sat=None, n_modes=int(src["modes"].shape[0]), n_real=int(src["coeffs"].shape[1]))
+        out = torch.zeros(2, dtype=torch.float64, device=dev)
+        j0, j1 = j_range if j_range is not None else (0, grid.ny)
+        main = torch.cuda.current_stream(dev)
+        copy = torch.cuda.Stream(dev)
+        copy.wait_stream(main)                       # the destination allocations
+        nt = grid.nt
+        bounds = [nt * i // max(1, min(slabs, nt)) for i in range(max(1, min(slabs, nt)) + 1)]
+        lib = _lib.load()
+        for t0, t1 in zip(bounds[:-1], bounds[1:]):
+            with torch.cuda.stream(copy):
+                dst["mean"][t0:t1].copy_(src["mean"][t0:t1], non_blocking=True)
+                for m in range(de.n_modes):          # [m][t] slabs: one contiguous run per mode
+                    dst["modes"][m, t0:t1].copy_(src["modes"][m, t0:t1], non_blocking=True)
+                dst["coeffs"][t0:t1].copy_(src["coeffs"][t0:t1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            main.wait_event(ev)
+            _lib.check(lib.fm_velocity_max_slab(de.fm_grid(), de.fm_env(), int(t0), int(t1), int(j0), int(j1),
+                                                out.data_ptr(), _lib.stream_ptr(main)), "fm_velocity_max_slab")
+        with torch.cuda.stream(copy):
+            dst["g"].copy_(src["g"], non_blocking=True)
+            dst["mask"].copy_(src["mask"], non_blocking=True)
+        main.wait_stream(copy)
+        for v in dst.values():                       # written on the copy stream, used on main
+            v.record_stream(copy)
+        de._make_sat()
+        de._scan = (out, tuple(j_range) if j_range is not None else None)
+        return de
+
     def _make_sat(self):
         torch = _torch()
         g = self.grid
@@ -112,6 +171,7 @@ class DeviceEnv:
         """Forget cached sub-grid / gate statistics (they are recomputed)."""
         self._vmax = None
         self._vbound = {}
+        self._scan = None
 
     def velocity_max(self, j_range: tuple | None = None, group=None) -> tuple:
         """Exact max |v_x|, |v_y| over (t, r, cell) -- compute_subgrid's scan.
@@ -119,6 +179,17 @@ class DeviceEnv:
         With ``j_range`` (this rank's row strip) and a process ``group``
         each rank scans its strip and the maxima are combined with one
         all-reduce (MAX) -- the same value as the full scan."""
+        if self._vmax is None and self._scan is not None and self._scan[1] == (
+                tuple(j_range) if j_range is not None else None):
+            out, scanned_rows = self._scan   # scanned slab by slab during the upload
+            self._scan = None
+            if scanned_rows is not None and (group is not None or _dist_world() > 1):
+                from .sharding import all_reduce_max
+                all_reduce_max(out, group)
+            h = out.cpu().numpy()
+            if scanned_rows is not None and not (group is not None or _dist_world() > 1):
+                return (float(h[0]), float(h[1]))   # a strip's maximum alone: never cached
+            self._vmax = (float(h[0]), float(h[1]))
         if self._vmax is None:
             torch = _torch()
             out = torch.zeros(2, dtype=torch.float64, device=self.mean.device)

@@ -190,12 +190,12 @@ __device__ __forceinline__ float2 ffma2_bcast(float a, float2 b, float2 c)
 static constexpr int kVmaxCells = 2;
 
 template <int NMX>
-__global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int cell0, int ncell, int r_per_block,
+__global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int cell0, int ncell, int r_per_block,
                                                const double *cmax, double *out2)
 {
     __shared__ float cs[kVmaxChunk][NMX];
     const int nc = G.nx * G.ny;
-    const int t = blockIdx.y;
+    const int t = t0 + blockIdx.y;   // cmax holds the slab's layers only
     const int nm = E.n_modes;
     const int r_lo = blockIdx.z * r_per_block;
     const int r_hi = min(E.n_real, r_lo + r_per_block);
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int cell0, in
                     const double2 md =
                         *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + c) * 2);
                     d32[q][m] = make_float2((float)md.x, (float)md.y);
-                    const double cm = cmax[(size_t)t * nm + m];
+                    const double cm = cmax[(size_t)(t - t0) * nm + m];
                     Tx += fabs(md.x) * cm;
                     Ty += fabs(md.y) * cm;
                 }
@@ -329,22 +329,31 @@ extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *st
 
 extern "C" int32_t fm_velocity_max_rows(fm_grid G, fm_env E, int32_t j0, int32_t j1, double *d_out2, void *stream)
 {
+    return fm_velocity_max_slab(G, E, 0, G.nt, j0, j1, d_out2, stream);
+}
+
+extern "C" int32_t fm_velocity_max_slab(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
+                                        double *d_out2, void *stream)
+{
     if (G.nx < 1 || G.ny < 1 || G.nt < 1 || E.n_real < 1 || E.n_modes < 0 || E.n_modes > 16)
         return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims (n_modes must be <= 16)");
     if (j0 < 0 || j1 > G.ny || j0 >= j1) return fm_fail(FM_BAD_ARG, "fm_velocity_max_rows: bad row range");
+    if (t0 < 0 || t1 > G.nt || t0 >= t1) return fm_fail(FM_BAD_ARG, "fm_velocity_max_slab: bad layer range");
     cudaStream_t s = (cudaStream_t)stream;
     pool_keep();
     const int nc = (j1 - j0) * G.nx;   // cells scanned
     const int nm = E.n_modes;
-    // max_r |coeff[t, r, m]| per (t, m): the error-bound ingredient
+    const int nts = t1 - t0;           // layers scanned
+    // max_r |coeff[t, r, m]| per (t, m) of the slab: the error-bound ingredient
     double *cmax = nullptr;
-    FM_CK(cudaMallocAsync(&cmax, sizeof(double) * (size_t)(G.nt * (nm > 0 ? nm : 1)), s));
+    FM_CK(cudaMallocAsync(&cmax, sizeof(double) * (size_t)(nts * (nm > 0 ? nm : 1)), s));
     if (nm > 0) {
-        k_maxabs_seg<<<G.nt * nm, 256, 0, s>>>(E.coeffs, E.n_real, nm, nm, (int64_t)E.n_real * nm, 1, cmax);
+        k_maxabs_seg<<<nts * nm, 256, 0, s>>>(E.coeffs + (size_t)t0 * E.n_real * nm, E.n_real, nm, nm,
+                                              (int64_t)E.n_real * nm, 1, cmax);
         FM_CK_LAUNCH("k_maxabs_seg");
     }
     const int bx = (nc + 256 * kVmaxCells - 1) / (256 * kVmaxCells);
-    long long base = (long long)bx * G.nt;
+    long long base = (long long)bx * nts;
     int rpb = E.n_real;
     const long long want = 4LL * sm_count();
     if (base < want) {
@@ -352,13 +361,13 @@ extern "C" int32_t fm_velocity_max_rows(fm_grid G, fm_env E, int32_t j0, int32_t
         rpb = (int)((E.n_real + split - 1) / split);
         rpb = ((rpb + kVmaxChunk - 1) / kVmaxChunk) * kVmaxChunk;
     }
-    dim3 grid(bx, G.nt, (E.n_real + rpb - 1) / rpb);
+    dim3 grid(bx, nts, (E.n_real + rpb - 1) / rpb);
     if (nm <= 4)
-        k_vmax<4><<<grid, 256, 0, s>>>(G, E, j0 * G.nx, nc, rpb, cmax, d_out2);
+        k_vmax<4><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2);
     else if (nm <= 8)
-        k_vmax<8><<<grid, 256, 0, s>>>(G, E, j0 * G.nx, nc, rpb, cmax, d_out2);
+        k_vmax<8><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2);
     else
-        k_vmax<16><<<grid, 256, 0, s>>>(G, E, j0 * G.nx, nc, rpb, cmax, d_out2);
+        k_vmax<16><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2);
     FM_CK_LAUNCH("k_vmax");
     FM_CK(cudaFreeAsync(cmax, s));
     return FM_OK;

@@ -37,7 +37,8 @@ def plan(env, actions, rcfg, target, buffer: int = 1, device_env: DeviceEnv | No
     """Size the sub-grid (k_vmax), build the model (k_build) and solve it
     backward in time (k_solve_layer).  Inputs already resident in HBM are
     reused through ``device_env``."""
-    denv = device_env if device_env is not None else DeviceEnv.from_host(env)
+    # host inputs: the exact scan runs slab by slab under the upload
+    denv = device_env if device_env is not None else DeviceEnv.from_host_scanned(env)
     sub = subgrid if subgrid is not None else subgrid_from_vmax(denv.velocity_max(), actions.f_max,
                                                                denv.grid, buffer)
     # the solve is queued behind the build; the build's census/overflow

@@ -389,3 +389,34 @@ def test_dense_random_obstacles(density):
     for obj in ("time", "energy", "net_energy"):
         rcfg = RewardConfig(obj, c_f=1.0, c_r=0.5, r_term=100.0, r_outbound=-300.0)
         _gpu_case(env, acts, rcfg, target)
+
+
+@pytest.mark.parametrize("slabs", [1, 3, 8, 64])
+def test_scanned_upload_matches_full_scan(slabs):
+    """DeviceEnv.from_host_scanned (slab-wise H2D with the exact scan of each
+    slab overlapping the next copy) uploads the same bytes and yields the
+    full scan's maxima bit for bit, for the whole grid and for a row strip."""
+    import torch
+    for env in (make_named_env("desk")[0], make_random_env(7009)[0], make_named_env("smoke")[0]):
+        ref = DeviceEnv.from_host(env)
+        full = ref.velocity_max()
+        de = DeviceEnv.from_host_scanned(env, slabs=slabs)
+        for k in ("mean", "modes", "coeffs", "g", "mask", "sat"):
+            assert torch.equal(getattr(de, k), getattr(ref, k)), k
+        got = de.velocity_max()
+        assert np.float64(got[0]).tobytes() == np.float64(full[0]).tobytes()
+        assert np.float64(got[1]).tobytes() == np.float64(full[1]).tobytes()
+        ny = env.grid.ny
+        j0, j1 = ny // 3, max(ny // 3 + 1, (2 * ny) // 3)
+        ref.reset_derived()
+        strip = ref.velocity_max(j_range=(j0, j1))
+        ds = DeviceEnv.from_host_scanned(env, slabs=slabs, j_range=(j0, j1))
+        assert ds.velocity_max(j_range=(j0, j1)) == strip
+        pinned = type("E", (), {})()   # pinned torch tensors, the e2e bench's inputs
+        pinned.grid = env.grid
+        pinned.field = type("F", (), {k: torch.from_numpy(np.ascontiguousarray(getattr(env.field, k))).pin_memory()
+                                      for k in ("mean", "modes", "coeffs")})()
+        pinned.scalar = type("S", (), {"g_mean": torch.from_numpy(env.scalar.g_mean).pin_memory()})()
+        pinned.obstacles = type("O", (), {"mask": torch.from_numpy(env.obstacles.mask.view(np.uint8)).pin_memory()})()
+        dp = DeviceEnv.from_host_scanned(pinned, slabs=slabs)
+        assert torch.equal(dp.modes, ref.modes) and dp.velocity_max() == full
