@@ -322,6 +322,61 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
 __global__ void k_maxabs_seg(const double *src, int64_t seg_len, int64_t elem_stride, int64_t inner,
                              int64_t outer_stride, int64_t inner_stride, double *out);
 
+// More than 16 modes: the plain f64 scan (the filter's per-cell mode
+// registers would not fit).  One thread per cell, RB realizations at a time,
+// modes outer so each mode is loaded once per block of realizations; every
+// realization's sum still runs in mode order (environment.py:293-297).
+template <int RB>
+__global__ void __launch_bounds__(256) k_vmax_f64(fm_grid G, fm_env E, int t0, int cell0, int ncell,
+                                                   int r_per_block, double *out2)
+{
+    const int nc = G.nx * G.ny;
+    const int t = t0 + blockIdx.y;
+    const int nm = E.n_modes;
+    const int lc = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = lc < ncell;
+    const int c = cell0 + (ok ? lc : 0);
+    const int r_lo = blockIdx.z * r_per_block;
+    const int r_hi = min(E.n_real, r_lo + r_per_block);
+    double ex = 0.0, ey = 0.0;
+    if (ok) {
+        const double2 mu = *reinterpret_cast<const double2 *>(E.mean + ((size_t)t * nc + c) * 2);
+        for (int r0 = r_lo; r0 < r_hi; r0 += RB) {
+            double vx[RB], vy[RB];
+#pragma unroll
+            for (int q = 0; q < RB; ++q) vx[q] = mu.x, vy[q] = mu.y;
+            for (int m = 0; m < nm; ++m) {
+                const double2 md = *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + c) * 2);
+#pragma unroll
+                for (int q = 0; q < RB; ++q) {
+                    const int r = min(r0 + q, r_hi - 1);   // past the end: a repeat, harmless for a max
+                    const double cf = __ldg(E.coeffs + ((size_t)t * E.n_real + r) * nm + m);
+                    vx[q] = DADD(vx[q], DMUL(cf, md.x));
+                    vy[q] = DADD(vy[q], DMUL(cf, md.y));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RB; ++q) {
+                const double ax = fabs(vx[q]), ay = fabs(vy[q]);
+                ex = (ax != ax || ax > ex) ? ax : ex;   // NaN sticks
+                ey = (ay != ay || ay > ey) ? ay : ey;
+            }
+        }
+    }
+    unsigned long long bx = (unsigned long long)__double_as_longlong(ex),
+                       by = (unsigned long long)__double_as_longlong(ey);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long ox = __shfl_xor_sync(kFull, bx, o), oy = __shfl_xor_sync(kFull, by, o);
+        bx = ox > bx ? ox : bx;
+        by = oy > by ? oy : by;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_nonneg(out2, __longlong_as_double((long long)bx));
+        atomic_max_nonneg(out2 + 1, __longlong_as_double((long long)by));
+    }
+}
+
 extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *stream)
 {
     return fm_velocity_max_rows(G, E, 0, G.ny, d_out2, stream);
@@ -335,8 +390,8 @@ extern "C" int32_t fm_velocity_max_rows(fm_grid G, fm_env E, int32_t j0, int32_t
 extern "C" int32_t fm_velocity_max_slab(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
                                         double *d_out2, void *stream)
 {
-    if (G.nx < 1 || G.ny < 1 || G.nt < 1 || E.n_real < 1 || E.n_modes < 0 || E.n_modes > 16)
-        return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims (n_modes must be <= 16)");
+    if (G.nx < 1 || G.ny < 1 || G.nt < 1 || E.n_real < 1 || E.n_modes < 0)
+        return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims");
     if (j0 < 0 || j1 > G.ny || j0 >= j1) return fm_fail(FM_BAD_ARG, "fm_velocity_max_rows: bad row range");
     if (t0 < 0 || t1 > G.nt || t0 >= t1) return fm_fail(FM_BAD_ARG, "fm_velocity_max_slab: bad layer range");
     cudaStream_t s = (cudaStream_t)stream;
@@ -344,6 +399,16 @@ extern "C" int32_t fm_velocity_max_slab(fm_grid G, fm_env E, int32_t t0, int32_t
     const int nc = (j1 - j0) * G.nx;   // cells scanned
     const int nm = E.n_modes;
     const int nts = t1 - t0;           // layers scanned
+    if (nm > 16) {
+        const int bxf = (nc + 255) / 256;
+        const long long basef = (long long)bxf * nts, want = 4LL * sm_count();
+        int rpb = E.n_real;
+        if (basef < want) rpb = (int)((E.n_real + (want + basef - 1) / basef - 1) / ((want + basef - 1) / basef));
+        if (rpb < 1) rpb = 1;
+        k_vmax_f64<8><<<dim3(bxf, nts, (E.n_real + rpb - 1) / rpb), 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, d_out2);
+        FM_CK_LAUNCH("k_vmax_f64");
+        return FM_OK;
+    }
     // max_r |coeff[t, r, m]| per (t, m) of the slab: the error-bound ingredient
     double *cmax = nullptr;
     FM_CK(cudaMallocAsync(&cmax, sizeof(double) * (size_t)(nts * (nm > 0 ? nm : 1)), s));

@@ -190,3 +190,34 @@ def test_huge_subgrid_global_histogram(objective):
     assert ores == 0.0
     vals, pol = solve_backward(build_device_model(ctx.device_env(), acts, rcfg, target, sub))
     assert sha(vals.cpu().numpy()) == sha(ov)
+
+
+@pytest.mark.parametrize("nm", [16, 17, 33, 64])
+def test_many_modes(nm):
+    """Mode counts past the FP32 filter's register budget (> 16: the plain f64
+    scan) and up to the build's 64: sub-grid, model and values bit-exact."""
+    rng = np.random.default_rng(nm)
+    nx, ny, nt, nr = 11, 9, 4, 70
+    g = GridSpec(nx=nx, ny=ny, nt=nt, dx=1.0, dt=1.0)
+    mask = np.zeros((nt, ny, nx), dtype=bool)
+    mask[:, 4, 3:6] = True
+    env = Environment(grid=g,
+                      field=DOVelocityField(mean=rng.normal(0, 0.6, (nt, ny, nx, 2)),
+                                            modes=rng.normal(0, 0.3, (nm, nt, ny, nx, 2)),
+                                            coeffs=rng.normal(0, 0.4, (nt, nr, nm))),
+                      scalar=ScalarMeanField(g_mean=rng.uniform(0, 2, (nt, ny, nx))),
+                      obstacles=ObstacleMask(mask=mask))
+    acts = ActionSpace(n_headings=8, n_speeds=1, f_max=1.0)
+    from paper_2109_00857_b200.builder import DeviceEnv
+    got, want = DeviceEnv.from_host(env).velocity_max(), O.velocity_max(env.field)
+    assert np.array(got).tobytes() == np.array(want, dtype=np.float64).tobytes()
+    for obj in ("time", "net_energy"):
+        rcfg = RewardConfig(obj, c_f=1.0, c_r=0.5, r_term=10.0, r_outbound=-30.0)
+        ctx = StepContext(env, acts, rcfg, (8, 7))
+        sub = fm.compute_subgrid(env.field, acts, env.grid)
+        hx, hy = O.compute_subgrid(env.field, acts.f_max, env.grid)
+        assert (sub.half_width_x, sub.half_width_y) == (hx, hy)
+        om = O.build_model(env, acts, rcfg, (8, 7), hx, hy)
+        assert model_digest(fm.build_model(ctx, sub)) == model_digest(om)
+        dmc = build_device_model(ctx.device_env(), acts, rcfg, (8, 7), sub, lean=False)
+        assert model_digest(dmc.to_sparse_model()) == model_digest(om)
