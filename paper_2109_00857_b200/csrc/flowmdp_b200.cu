@@ -2083,7 +2083,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     const fm_grid &G = h->grid;
     if (G.nx < 1 || G.ny < 1 || G.nt < 1 || !(G.dx > 0) || !(G.dt > 0))
         return fm_fail(FM_BAD_ARG, "fm_build: bad grid");
-    if (h->env.n_modes < 0 || h->env.n_modes > 64) return fm_fail(FM_BAD_ARG, "fm_build: n_modes must be in [0,64]");
+    if (h->env.n_modes < 0 || h->env.n_modes > 512) return fm_fail(FM_BAD_ARG, "fm_build: n_modes must be in [0,512]");
     if (h->env.n_real < 1 || h->env.n_real > 65535) return fm_fail(FM_BAD_ARG, "fm_build: n_real must be in [1,65535]");
     if (h->n_actions < 1) return fm_fail(FM_BAD_ARG, "fm_build: need >= 1 action");
     if (h->hx < 0 || h->hy < 0) return fm_fail(FM_BAD_ARG, "fm_build: negative sub-grid");

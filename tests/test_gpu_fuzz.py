@@ -192,10 +192,11 @@ def test_huge_subgrid_global_histogram(objective):
     assert sha(vals.cpu().numpy()) == sha(ov)
 
 
-@pytest.mark.parametrize("nm", [16, 17, 33, 64])
+@pytest.mark.parametrize("nm", [16, 17, 33, 64, 100, 200])
 def test_many_modes(nm):
     """Mode counts past the FP32 filter's register budget (> 16: the plain f64
-    scan) and up to the build's 64: sub-grid, model and values bit-exact."""
+    scan) and into the hundreds (the build stages them in shared memory with a
+    smaller chunk): sub-grid, model and values bit-exact."""
     rng = np.random.default_rng(nm)
     nx, ny, nt, nr = 11, 9, 4, 70
     g = GridSpec(nx=nx, ny=ny, nt=nt, dx=1.0, dt=1.0)
