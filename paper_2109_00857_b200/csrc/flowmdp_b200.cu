@@ -188,6 +188,10 @@ __device__ __forceinline__ float2 ffma2_bcast(float a, float2 b, float2 c)
 // two FFMA2 chains; the running exact maxima are shared by the two cells
 // (an element can only raise the global maximum if |v32| >= E - delta_cell).
 static constexpr int kVmaxCells = 2;
+#ifndef FM_VMAX_STEP
+#define FM_VMAX_STEP 4
+#endif
+static constexpr int kVmaxStep = FM_VMAX_STEP;   // realizations per step
 
 template <int NMX>
 __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int cell0, int ncell, int r_per_block,
@@ -252,45 +256,50 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
         }
         __syncthreads();
         if (!ok[0]) continue;
-        // two realizations per step; (vx, vy) in one packed FFMA2 chain.
+        // kVmaxStep realizations per step; (vx, vy) in one packed FFMA2 chain.
         // Unused modes hold zeros (exact no-ops), so no mode-count test.
-        // chunks hold an even count except possibly the last (n odd: the
-        // second lane of the pair re-evaluates realization k, harmless)
-        for (int k = 0; k < n; k += 2) {
-            const int k1 = k + 1 < n ? k + 1 : k;
-            float2 v0[kVmaxCells], v1[kVmaxCells];
+        // A step past the chunk's end re-evaluates its last realization
+        // (harmless for a maximum).
+        for (int k = 0; k < n; k += kVmaxStep) {
+            int kk[kVmaxStep];
 #pragma unroll
-            for (int q = 0; q < kVmaxCells; ++q) v0[q] = v1[q] = mu32[q];
+            for (int j = 0; j < kVmaxStep; ++j) kk[j] = min(k + j, n - 1);
+            float2 v[kVmaxStep][kVmaxCells];
+#pragma unroll
+            for (int j = 0; j < kVmaxStep; ++j)
+#pragma unroll
+                for (int q = 0; q < kVmaxCells; ++q) v[j][q] = mu32[q];
 #pragma unroll
             for (int m = 0; m < NMX; ++m) {
-                const float c0 = cs[k][m], c1 = cs[k1][m];
 #pragma unroll
-                for (int q = 0; q < kVmaxCells; ++q) {
-                    v0[q] = ffma2_bcast(c0, d32[q][m], v0[q]);
-                    v1[q] = ffma2_bcast(c1, d32[q][m], v1[q]);
+                for (int j = 0; j < kVmaxStep; ++j) {
+                    const float cj = cs[kk[j]][m];
+#pragma unroll
+                    for (int q = 0; q < kVmaxCells; ++q) v[j][q] = ffma2_bcast(cj, d32[q][m], v[j][q]);
                 }
             }
             // !(|v| < th) also routes NaN / inf to the exact path
             bool hit = false;
 #pragma unroll
-            for (int q = 0; q < kVmaxCells; ++q)
-                hit = hit || !(fabsf(v0[q].x) < thx[q]) || !(fabsf(v0[q].y) < thy[q]) ||
-                      !(fabsf(v1[q].x) < thx[q]) || !(fabsf(v1[q].y) < thy[q]);
+            for (int j = 0; j < kVmaxStep; ++j)
+#pragma unroll
+                for (int q = 0; q < kVmaxCells; ++q)
+                    hit = hit || !(fabsf(v[j][q].x) < thx[q]) || !(fabsf(v[j][q].y) < thy[q]);
             if (hit) {
 #pragma unroll
                 for (int q = 0; q < kVmaxCells; ++q) {
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const float2 v = j ? v1[q] : v0[q];
-                        const int r = r0 + (j ? k1 : k);
-                        if (!(fabsf(v.x) < thx[q])) {
+                    for (int j = 0; j < kVmaxStep; ++j) {
+                        const float2 vv = v[j][q];
+                        const int r = r0 + kk[j];
+                        if (!(fabsf(vv.x) < thx[q])) {
                             const double e = vmax_exact_component<NMX>(G, E, t, r, cell[q], 0);
                             ex = (e != e || e > ex) ? e : ex;   // NaN sticks (the reference's max propagates it)
 #pragma unroll
                             for (int qq = 0; qq < kVmaxCells; ++qq)
                                 if (ok[qq]) thx[qq] = __double2float_rd(ex - delx[qq]);
                         }
-                        if (!(fabsf(v.y) < thy[q])) {
+                        if (!(fabsf(vv.y) < thy[q])) {
                             const double e = vmax_exact_component<NMX>(G, E, t, r, cell[q], 1);
                             ey = (e != e || e > ey) ? e : ey;
 #pragma unroll
