@@ -133,7 +133,14 @@ def cpu_sample(w, env, seconds: float, threads: int):
                   j_range=(j0, j1))
     dt = time.perf_counter() - t0
     units = n_slabs * (j1 - j0) * g.nx * w.n_actions * w.n_realizations
-    desc = (f"oracle build (C restatement of model_builder.build_model, -O2, no FMA) on slabs "
+    cpu_model = "unknown CPU"
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), cpu_model)
+    except OSError:
+        pass
+    desc = (f"[{cpu_model}, os.cpu_count()={os.cpu_count()}] "
+            f"oracle build (C restatement of model_builder.build_model, -O2, no FMA) on slabs "
             f"t=[{t_lo},{t_lo + n_slabs}) x rows j=[{j0},{j1}) of {w.name}: {units:.3e} transitions in "
             f"{dt:.1f}s on {threads} threads; solve excluded (reference VI is <1% of its build)")
     return units / dt, desc, threads
