@@ -42,7 +42,7 @@ def _args():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default=WORKLOAD)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
+    p.add_argument("--cpu-seconds", type=float, default=25.0, help="target CPU-baseline sample length")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo: validation of the N>1 path with several ranks on one GPU (halo and maxima "
                         "staged through host memory); never a bench number")
