@@ -251,6 +251,12 @@ int32_t fm_solve_backward(const fm_model *h_model, int32_t t_lo, int32_t t_hi,
 /* One backward layer restricted to rows j in [j0, j1) (multi-GPU strips). */
 int32_t fm_solve_layer(const fm_model *h_model, int32_t t, int32_t j0, int32_t j1,
                        double *values, uint16_t *policy, void *stream);
+/* The count -> probability table fl(q / n_real), q = 0..n_real, into
+ * d_ptab [n_real + 1] -- built once per model so a strip solve's layers
+ * (fm_solve_layer_tab) launch one kernel each. */
+int32_t fm_prob_table(int32_t n_real, double *d_ptab, void *stream);
+int32_t fm_solve_layer_tab(const fm_model *h_model, const double *d_ptab, int32_t t, int32_t j0, int32_t j1,
+                           double *values, uint16_t *policy, void *stream);
 
 /* General CSR (explicit f64 probabilities) for host-supplied models
  * (io.read_model widens f32 vals, io.py:280-292): per action a, rows of

@@ -140,6 +140,9 @@ SIGNATURES = {
                                       C.c_void_p]),
     "fm_solve_layer": (C.c_int32, [C.POINTER(FmModel), C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                    C.c_void_p, C.c_void_p]),
+    "fm_prob_table": (C.c_int32, [C.c_int32, C.c_void_p, C.c_void_p]),
+    "fm_solve_layer_tab": (C.c_int32, [C.POINTER(FmModel), C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
     "fm_csr_row_ptr": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p,
                                    C.c_void_p, C.c_void_p]),
     "fm_jacobi": (C.c_int32, [C.POINTER(FmCsr), C.c_double, C.c_int32, C.c_void_p, C.c_void_p,

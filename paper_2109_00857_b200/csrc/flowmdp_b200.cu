@@ -2563,6 +2563,22 @@ extern "C" int32_t fm_solve_layer(const fm_model *M, int32_t t, int32_t j0, int3
     return FM_OK;
 }
 
+extern "C" int32_t fm_prob_table(int32_t n_real, double *d_ptab, void *stream)
+{
+    if (n_real < 1 || !d_ptab) return fm_fail(FM_BAD_ARG, "fm_prob_table: bad arguments");
+    k_prob_table<<<(n_real + 256) / 256, 256, 0, (cudaStream_t)stream>>>(d_ptab, n_real);
+    FM_CK_LAUNCH("k_prob_table");
+    return FM_OK;
+}
+
+extern "C" int32_t fm_solve_layer_tab(const fm_model *M, const double *d_ptab, int32_t t, int32_t j0, int32_t j1,
+                                      double *values, uint16_t *policy, void *stream)
+{
+    if (t < 0 || t >= M->nt || j0 < 0 || j1 > M->ny || j0 >= j1 || !d_ptab)
+        return fm_fail(FM_BAD_ARG, "fm_solve_layer_tab: bad range");
+    return solve_layer(M, d_ptab, t, j0, j1, values, policy, (cudaStream_t)stream);
+}
+
 // ---------------------------------------------------------------------------
 // general CSR path (host-supplied SparseModel): Jacobi VI, greedy, policy
 // ---------------------------------------------------------------------------

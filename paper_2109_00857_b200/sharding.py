@@ -114,13 +114,23 @@ def solve_sharded(layer_fn, values, nt: int, nx: int, ny: int, hy: int, group=No
 
 
 def device_solve_sharded(dmodel, values, policy, j0: int, j1: int, group=None) -> int:
-    """GPU strip solve: k_solve_layer per t + NCCL halo exchange."""
-    from .solver import solve_layer
+    """GPU strip solve: k_solve_layer per t + NCCL halo exchange (the
+    count -> probability table is built once for all layers)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
 
     g = dmodel.grid
     hy = dmodel.subgrid.half_width_y
+    L = _lib.load()
+    m = dmodel.fm_model()
+    ptab = torch.empty(dmodel.n_real + 1, dtype=torch.float64, device=values.device)
+    _lib.check(L.fm_prob_table(int(dmodel.n_real), ptab.data_ptr(), _lib.stream_ptr()), "fm_prob_table")
 
     def layer(t):
-        solve_layer(dmodel, t, j0, j1, values, policy)
+        _lib.check(L.fm_solve_layer_tab(C.byref(m), ptab.data_ptr(), int(t), int(j0), int(j1), values.data_ptr(),
+                                        policy.data_ptr(), _lib.stream_ptr()), "fm_solve_layer_tab")
 
     return solve_sharded(layer, values, g.nt, g.nx, g.ny, hy, group)
