@@ -375,12 +375,12 @@ def run_ours(args):
     # upper bound on the bytes this kernel needs
     n_rows_rank = (j1 - j0) * g.nx * g.nt * w.n_actions
     solve_bytes = 12 * build_ev[-1][2] + 8 * n_rows_rank + 18 * (j1 - j0) * g.nx * g.nt
-    hbm_peak, hbm_src = 6650.0, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
+    hbm_peak, hbm_src = 6650.0, "B200_PROFILING.md fallback (no HBM figure in MEASURED_PEAKS.json)"
     mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(mp):
         try:
             pk = json.load(open(mp))
-            for key in ("hbm_gbps", "hbm_GBps", "hbm_copy_gbps", "hbm_burst_gbps"):
+            for key in ("hbm_gbs", "hbm_gbps", "hbm_GBps", "hbm_copy_gbps", "hbm_burst_gbps"):
                 if key in pk:
                     hbm_peak, hbm_src = float(pk[key]), f"MEASURED_PEAKS.json:{key}"
                     break
