@@ -2436,12 +2436,25 @@ __global__ void k_prob_table(double *ptab, int nr)
     if (k <= nr) ptab[k] = DDIV((double)k, (double)nr);
 }
 
+#ifndef FM_SOLVE_PDL
+#define FM_SOLVE_PDL 1
+#endif
+
 __global__ void __launch_bounds__(256) k_solve_layer(const SolveK S)
 {
     extern __shared__ int soff[];   // slot -> dj*nx + di
     const ModelK &K = S.M;
+#if FM_SOLVE_PDL
+    // programmatic dependent launch: the next layer's blocks may be scheduled
+    // now; they run their prologue and then wait (griddepcontrol.wait) for
+    // this grid to complete and its V / policy writes to be visible
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     for (int k = threadIdx.x; k < K.nslot; k += blockDim.x)
         soff[k] = (k / K.width - K.hy) * K.nx + (k % K.width - K.hx);
+#if FM_SOLVE_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // nothing above reads device data
+#endif
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int grp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -2512,7 +2525,22 @@ static int32_t solve_layer(const fm_model *M, const double *ptab, int t, int j0,
     const int wpb = 8;
     const unsigned nb = (unsigned)((S.groups + wpb - 1) / wpb);
     const size_t smem = sizeof(int) * (size_t)S.M.nslot;
+#if FM_SOLVE_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(wpb * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, k_solve_layer, S);
+    if (le != cudaSuccess) return fm_fail(FM_CUDA_ERROR, "launch k_solve_layer: %s", cudaGetErrorString(le));
+#else
     k_solve_layer<<<nb, wpb * 32, smem, s>>>(S);
+#endif
     FM_CK_LAUNCH("k_solve_layer");
     return FM_OK;
 }
