@@ -1845,11 +1845,21 @@ static void smem_layout_fit(BuildK &K, int queue, bool hg)
             smem_sm = 233472;
         cudaGetLastError();
     }
+    // resident warps per SM with 4-warp blocks (capped at 16); more warps
+    // win, the larger chunk on a tie (wide sub-grids: neither fits 16 warps
+    // and the 64-realization chunk measured faster, 98.9 vs 111.0 ms)
     const int cands[2] = {K.RW >= FM_BUILD_RC ? K.RW : FM_BUILD_RC, K.RW >= 32 ? K.RW : 32};
+    int best = 0, best_w = -1;
     for (int i = 0; i < 2; ++i) {
         smem_layout(K, cands[i], queue, hg);
-        if (smem_sm / (4 * K.smem_warp + 1024) >= 4) return;
+        int blocks = smem_sm / (4 * K.smem_warp + 1024);
+        if (blocks > 4) blocks = 4;
+        if (4 * blocks > best_w) {
+            best_w = 4 * blocks;
+            best = i;
+        }
     }
+    smem_layout(K, cands[best], queue, hg);
 }
 
 template <int FL, int PART>
