@@ -9,12 +9,25 @@ value_iteration (pipeline.py:96-136) without file I/O.
   value : transitions/s = U / step time, U = N_c * nt * |A| * N_rv, inputs
           resident in HBM, device time (CUDA events), max over ranks.
   e2e   : the same metric through the public API from pinned HOST inputs:
-          H2D of mean/modes/coeffs/g/mask + the step + D2H of values/policy.
+          H2D of mean/modes/coeffs/g/mask + the step + D2H of everything the
+          planner produces -- values, policy AND the compact transition model
+          (row pointers, entry counts, rewards, entries).
+  e2e_dropin : the reference callers' path (pipeline.run_build/run_solve
+          without files): compute_subgrid + build_model -> host SparseModel
+          (blocks[a][t] COO) + value_iteration(SparseModel) -> PolicyValue,
+          host wall clock.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-Multi-GPU: launched by torchrun; source rows are split into y-strips (one
-per rank), the solve exchanges a one-sub-grid-wide halo of V_{t+1} per
-layer over NCCL (strong scaling of the fixed C2 problem).
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under torch.distributed.run with N ranks (one per GPU).  Source rows are
+split into y-strips (one per rank), the solve exchanges a one-sub-grid-wide
+halo of V_{t+1} per layer over NCCL (strong scaling of the fixed C2 problem).
+
+--impl reference: the reference's CPU path on the host cores (rank 0 only):
+the oracle port (oracle/flowmdp_oracle.c) on a stratified sample -- every
+source row of slabs t in {0, nt/3, 2nt/3}, scan + build + value iteration
+-- each step; plus, once, the unmodified numpy reference (baseline/_ref) on
+a realization-cropped sample at 1 process and at all cores.
 """
 
 from __future__ import annotations
@@ -42,7 +55,6 @@ def _args():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default=WORKLOAD)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=25.0, help="target CPU-baseline sample length")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo: validation of the N>1 path with several ranks on one GPU (halo and maxima "
                         "staged through host memory); never a bench number")
@@ -103,71 +115,78 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle (C restatement of the reference) on host cores
+# CPU baselines (oracle/cpu_sample.py): the reference's CPU path on host cores
 # ---------------------------------------------------------------------------
 
-def cpu_sample(w, env, seconds: float, threads: int):
-    """Time the oracle build on a bounded sample of the workload: the same
-    slabs x source-row strip, all actions, all realizations.  Returns
-    (transitions/s, description, threads)."""
+def _cpu_sample_mod():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
+    import cpu_sample
+    return cpu_sample
 
+
+def config_of(w, world: int, backend: str = "nccl") -> dict:
+    """The workload description both arms print (same keys, same values)."""
     g = w.grid
-    # the exact sub-grid of the named workloads is pinned by tests (oracle /
-    # GPU); recomputing it on the CPU would dominate a bounded sample
-    hx, hy = w.subgrid_hint if w.subgrid_hint else O.compute_subgrid(env.field, w.f_max, g)
-    acts, rcfg = w.actions(), w.reward_config()
-    # calibrate: one row of one slab on one thread
-    t0 = time.perf_counter()
-    O.build_model(env, acts, rcfg, w.target, hx, hy, n_threads=1, t_range=(g.nt // 2, g.nt // 2 + 1),
-                  j_range=(g.ny // 2, g.ny // 2 + 1))
-    per_row = max(time.perf_counter() - t0, 1e-4)
-    rows = max(1, min(g.ny, int(seconds / per_row)))
-    n_slabs = max(1, min(threads, g.nt - 1))
-    j0 = max(0, g.ny // 2 - rows // 2)
-    j1 = min(g.ny, j0 + rows)
-    t_lo = max(0, g.nt // 2 - n_slabs // 2)
-    t0 = time.perf_counter()
-    O.build_model(env, acts, rcfg, w.target, hx, hy, n_threads=threads, t_range=(t_lo, t_lo + n_slabs),
-                  j_range=(j0, j1))
-    dt = time.perf_counter() - t0
-    units = n_slabs * (j1 - j0) * g.nx * w.n_actions * w.n_realizations
-    cpu_model = "unknown CPU"
-    try:
-        with open("/proc/cpuinfo") as f:
-            cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), cpu_model)
-    except OSError:
-        pass
-    desc = (f"[{cpu_model}, os.cpu_count()={os.cpu_count()}] "
-            f"oracle build (C restatement of model_builder.build_model, -O2, no FMA) on slabs "
-            f"t=[{t_lo},{t_lo + n_slabs}) x rows j=[{j0},{j1}) of {w.name}: {units:.3e} transitions in "
-            f"{dt:.1f}s on {threads} threads; solve excluded (reference VI is <1% of its build)")
-    return units / dt, desc, threads
+    return {"workload": w.name, "grid": [g.nx, g.ny, g.nt], "actions": w.n_actions,
+            "realizations": w.n_realizations, "modes": w.n_modes, "objective": w.objective,
+            "transitions": w.transitions,
+            "parallelism": f"ystrips{world}" + ("-gloo-validation" if backend == "gloo" else ""),
+            "l2": "flushed between steps (256 MiB write); inputs 185 MB > L2"}
+
+
+def cpu_baseline(w, env, subgrid=None) -> dict:
+    """One stratified oracle-port step on every host core (the GPU arm's
+    cpu_baseline: rank 0, N=1)."""
+    CS = _cpu_sample_mod()
+    threads = os.cpu_count() or 1
+    r = CS.port_step(w, env, threads, subgrid=subgrid or w.subgrid_hint)
+    return {"value": r["units"] / r["seconds"], "unit": "transitions/s", "cores": r["threads"], "kind": "port",
+            "sample": CS.port_description(r, w), "seconds": r["seconds"],
+            "full_step_s_extrapolated": r["full_step_s_extrapolated"]}
 
 
 def run_reference(args):
+    """The reference arm: rank 0 only (other ranks exit without work).
+
+    Each of the W + K steps is one sampled planner step of the oracle port
+    (scan + build + value iteration of three stratified slabs, all rows, all
+    realizations, all host cores); the line's value is the transitions/s of
+    the K timed steps.  ms_per_step is the measured duration of a step (of
+    the sample); the full-step time is extrapolated separately and says so.
+    The unmodified numpy reference is timed once on a smaller sample."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2109_00857_b200 import workloads
+    CS = _cpu_sample_mod()
     w = workloads.get(args.workload)
     env = w.environment()
     threads = os.cpu_count() or 1
-    vals = []
-    desc = ""
-    per_step = max(2.0, 60.0 / max(args.steps, 1))
-    for _ in range(args.steps):
-        v, desc, threads = cpu_sample(w, env, per_step, threads)
-        vals.append(v)
-    value = statistics.median(vals)
+    runs = []
+    for it in range(args.warmup + args.steps):
+        r = CS.port_step(w, env, threads, subgrid=w.subgrid_hint)
+        if it >= args.warmup:
+            runs.append(r)
+    units = sum(r["units"] for r in runs)
+    seconds = sum(r["seconds"] for r in runs)
+    value = units / seconds
+    numpy_ref = None
+    try:
+        numpy_ref = CS.numpy_reference(w, env, ROOT)
+    except Exception as exc:   # the supplementary numbers never fail the arm
+        numpy_ref = {"error": f"{type(exc).__name__}: {exc}"}
     line = {
         "impl": "reference", "metric": "transitions_per_s", "value": value, "unit": "transitions/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": w.transitions / value * 1e3,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": seconds / len(runs) * 1e3,
+        "ms_per_step_note": "measured duration of one sampled step (3 of nt slabs, every row); not extrapolated",
+        "full_step_ms_extrapolated": value and w.transitions / value * 1e3, "extrapolated_keys": ["full_step_ms_extrapolated"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "grid": [w.grid.nx, w.grid.ny, w.grid.nt], "actions": w.n_actions,
-                   "realizations": w.n_realizations, "objective": w.objective, "transitions": w.transitions},
-        "cpu_baseline": {"value": value, "unit": "transitions/s", "cores": threads, "kind": "port", "sample": desc},
+        "config": config_of(w, args.gpus, args.dist_backend),
+        "stages_s_median": {k: statistics.median(r[k] for r in runs) for k in ("scan_s", "build_s", "vi_s")},
+        "cpu_baseline": {"value": value, "unit": "transitions/s", "cores": runs[0]["threads"], "kind": "port",
+                         "sample": CS.port_description(runs[0], w)},
+        "numpy_reference": numpy_ref,
         "e2e": {"value": value, "unit": "transitions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -201,12 +220,14 @@ def run_ours(args):
     import paper_2109_00857_b200 as fm
     from paper_2109_00857_b200 import _lib, workloads
     from paper_2109_00857_b200.builder import DeviceEnv, build_device_model, subgrid_from_vmax
-    from paper_2109_00857_b200.sharding import all_reduce_max, device_solve_sharded, strip_bounds
+    from paper_2109_00857_b200.sharding import all_reduce_max, all_reduce_sum, device_solve_sharded, strip_bounds
     from paper_2109_00857_b200.solver import solve_backward
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.dist_backend == "gloo":   # ranks may share a GPU
         local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
@@ -237,6 +258,33 @@ def run_ours(args):
     build_ev = []
     prev = {}
 
+    def solve(dm):
+        if world > 1:
+            values.zero_()
+            device_solve_sharded(dm, values, policy, j0, j1)
+        else:
+            solve_backward(dm, values, policy)
+
+    def finish(dm):
+        """Deferred build check, collective-safe: every rank learns whether
+        any rank had to rebuild (capacity) or failed (sub-grid violation), so
+        all ranks re-run the halo-exchanging solve together or all raise."""
+        err, rebuilt = None, False
+        try:
+            rebuilt = dm.check()
+        except Exception as exc:   # re-raised after the ranks agree
+            err = exc
+        if world > 1:
+            flag = torch.tensor([float(rebuilt), float(err is not None)], dtype=torch.float64, device="cuda")
+            all_reduce_max(flag)
+            if flag[1].item() and err is None:
+                raise RuntimeError("k_build check failed on another rank")
+            rebuilt = bool(flag[0].item())
+        if err is not None:
+            raise err
+        if rebuilt:   # capacity miss somewhere: the model was rebuilt, solve again
+            solve(dm)
+
     def step(de, scanned=False):
         if not scanned:
             de.reset_derived()                   # sub-grid and gate statistics are recomputed every step
@@ -250,19 +298,10 @@ def run_ours(args):
                                 reuse=prev.pop("dm", None))   # the previous step's buffers: no allocation
         prev["dm"] = dm
         b1.record()
-        if world > 1:
-            values.zero_()
-            device_solve_sharded(dm, values, policy, j0, j1)
-        else:
-            solve_backward(dm, values, policy)
+        solve(dm)
         s1 = ev()
         s1.record()
-        if dm.check():                           # capacity miss: rebuilt, solve again
-            if world > 1:
-                values.zero_()
-                device_solve_sharded(dm, values, policy, j0, j1)
-            else:
-                solve_backward(dm, values, policy)
+        finish(dm)
         build_ev.append((b0, b1, dm.nnz, s1))
         return dm
 
@@ -312,10 +351,19 @@ def run_ours(args):
         obstacles = type("O", (), {"mask": pinned["mask"]})()
 
     h2d = sum(t.numel() * t.element_size() for t in pinned.values())
-    d2h = 0
     host_v = torch.empty(n_g + 1, dtype=torch.float64).pin_memory()
     host_p = torch.empty(n_g, dtype=torch.int16).pin_memory()
-    e2e_times = []
+    # the compact transition model comes out too (north_star: "transition
+    # model plus value function and policy out"): row pointers, entry counts,
+    # rewards of this rank's rows and its entries, on a copy stream that
+    # overlaps the solve
+    mdl = prev["dm"]
+    host_m = {"row_ptr": torch.empty_like(mdl.row_ptr, device="cpu").pin_memory(),
+              "row_nnz": torch.empty_like(mdl.row_nnz, device="cpu").pin_memory(),
+              "reward": torch.empty_like(mdl.reward, device="cpu").pin_memory(),
+              "entries": torch.empty(int(mdl.entries.numel()), dtype=torch.int32).pin_memory()}
+    d2h_stream = torch.cuda.Stream()
+    e2e_times, d2h_counts = [], []
     for it in range(args.warmup + args.steps):
         flush.zero_()
         barrier()
@@ -325,28 +373,70 @@ def run_ours(args):
         # upload in time slabs, the exact sub-grid scan of each slab overlapping
         # the next slab's copy (the planner's host-input path)
         de = DeviceEnv.from_host_scanned(_HostEnv, j_range=(j0, j1) if world > 1 else None)
-        step(de, scanned=True)
+        dm = step(de, scanned=True)
+        built = build_ev[-1][1]
+        rows_sl = slice(None)
+        d2h_stream.wait_event(built)
+        nbytes = 0
+        with torch.cuda.stream(d2h_stream):
+            for k in ("row_ptr", "row_nnz", "reward"):
+                host_m[k][rows_sl].copy_(getattr(dm, k)[rows_sl], non_blocking=True)
+                nbytes += getattr(dm, k)[rows_sl].numel() * getattr(dm, k).element_size()
+            if host_m["entries"].numel() < dm.nnz:   # a capacity retry grew the model
+                host_m["entries"] = torch.empty(int(dm.entries.numel()), dtype=torch.int32).pin_memory()
+            host_m["entries"][: dm.nnz].copy_(dm.entries[: dm.nnz], non_blocking=True)
+            nbytes += dm.nnz * 4
         if world == 1:
             host_v.copy_(values, non_blocking=True)
             host_p.copy_(policy, non_blocking=True)
+            nbytes += (n_g + 1) * 8 + n_g * 2
         else:
             lo, hi = j0 * g.nx, j1 * g.nx
             for t_ in range(g.nt):   # this rank's strip of every layer
                 a_, b_ = t_ * g.nx * g.ny + lo, t_ * g.nx * g.ny + hi
                 host_v[a_:b_].copy_(values[a_:b_], non_blocking=True)
                 host_p[a_:b_].copy_(policy[a_:b_], non_blocking=True)
+            nbytes += (j1 - j0) * g.nx * g.nt * (8 + 2)
+        torch.cuda.current_stream().wait_stream(d2h_stream)
         e1.record()
         torch.cuda.synchronize()
         barrier()
         if it >= args.warmup:
             e2e_times.append(e0.elapsed_time(e1))
-    d2h = (j1 - j0) * g.nx * g.nt * (8 + 2) + (8 if world == 1 else 0)
+            d2h_counts.append(nbytes)
+    d2h = int(statistics.median(d2h_counts))
     e2e_ms = sum(e2e_times)
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         all_reduce_max(t)
         e2e_ms = float(t.item())
+        t = torch.tensor([float(d2h)], dtype=torch.float64, device="cuda")
+        all_reduce_sum(t)
+        d2h_total = int(t.item())
+    else:
+        d2h_total = d2h
     e2e_value = w.transitions / (e2e_ms / args.steps / 1e3)
+
+    # ---- the reference callers' drop-in path (world 1: a host SparseModel) ----
+    dropin = None
+    if world == 1:
+        from paper_2109_00857_b200 import StepContext
+        dts = []
+        for it in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx = StepContext(env, acts, rcfg, w.target)
+            sub = fm.compute_subgrid(env.field, acts, g, buffer=w.buffer, device_env=ctx.device_env())
+            sm = fm.build_model(ctx, sub)
+            pv = fm.value_iteration(sm)
+            dts.append(time.perf_counter() - t0)
+            del sm, ctx
+        dt_ = statistics.median(dts[1:])
+        dropin = {"value": w.transitions / dt_, "unit": "transitions/s", "ms_per_step": dt_ * 1e3,
+                  "path": "StepContext -> compute_subgrid -> build_model -> host SparseModel (blocks[a][t] COO, "
+                          "f64 vals) -> value_iteration(SparseModel) (Jacobi, reference semantics) -> PolicyValue; "
+                          "host wall clock, numpy inputs (pageable), 1 warm-up + 2 timed",
+                  "jacobi_iterations": pv.iterations_run, "residual": pv.residual}
 
     # ---- roofline of the dominant kernel (k_build): FP64 pipe ------------------
     peak = fp64_peak(L, torch, s)
@@ -367,6 +457,9 @@ def run_ours(args):
                     "ncu_issue_active_pct_lean_part": pj.get("issue_active_pct_first")}
         except Exception:
             traffic = None
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    clocks = clk.summary()
+    ceiling = sm_count * 64 * (clocks["sm_mhz"] or 1965.0) * 1e6   # FP64 lanes per SM per clock x f_clk
 
     # backward solve against HBM: 12 B per entry (4 B column
     # + 8 B probability), 8 B reward per (state, action) row, 18 B per state
@@ -391,24 +484,29 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            v, desc, thr = cpu_sample(w, env, args.cpu_seconds, os.cpu_count() or 1)
-            cpu = {"value": v, "unit": "transitions/s", "cores": thr, "kind": "port", "sample": desc}
+            sg = prev["dm"].subgrid
+            cpu = cpu_baseline(w, env, subgrid=(sg.half_width_x, sg.half_width_y))
         line = {
             "metric": "transitions_per_s", "value": value, "unit": "transitions/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "grid": [g.nx, g.ny, g.nt], "actions": w.n_actions,
-                       "realizations": w.n_realizations, "modes": w.n_modes, "objective": w.objective,
-                       "transitions": w.transitions, "parallelism": f"ystrips{world}" + ("-gloo-validation" if args.dist_backend == "gloo" else ""),
-                       "l2": "flushed between steps (256 MiB write); inputs 185 MB > L2"},
+            "config": config_of(w, world, args.dist_backend),
             "stages": {"build_ms_median": build_ms, "solve_ms_median": solve_ms, "step_ms": ms_per_step,
                        "nnz": build_ev[-1][2]},
             "e2e": {"value": e2e_value, "unit": "transitions/s", "h2d_bytes_per_step": h2d * world,
-                    "d2h_bytes_per_step": d2h * world, "ms_per_step": e2e_ms / args.steps},
+                    "d2h_bytes_per_step": d2h_total, "ms_per_step": e2e_ms / args.steps,
+                    "path": "pinned host inputs -> DeviceEnv.from_host_scanned (slab-wise H2D + exact scan) -> "
+                            "build -> backward solve -> D2H of values, policy and the compact model (row_ptr, "
+                            "row_nnz, reward, entries)"},
+            "e2e_dropin": dropin,
             "roofline": {"bound": "fp64", "kernel": "k_build", "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": "fm_fp64_probe in this run (DADD+DMUL issue rate); MEASURED_PEAKS.json "
                                         "has no FP64 figure",
+                         "fp64_issue_ceiling": ceiling / 1e12,
+                         "fp64_issue_ceiling_note": f"{sm_count} SMs x 64 FP64 lanes/clk x the median SM clock "
+                                                   "under load (no-FMA ops)",
+                         "frac_of_ceiling": achieved / ceiling,
                          "flops_per_transition": flops_per_transition,
                          "flops_note": "algorithmic count of SURVEY.md 8(d) (13 + 4 N_m/|A|); the kernel executes "
                                        "fewer (identity ops skipped, floor as one DADD, count-formed rewards: "
@@ -419,7 +517,7 @@ def run_ours(args):
                                "bytes_algorithmic": solve_bytes, "ms": solve_ms, "peak_source": hbm_src,
                                "note": "nt dependent layers: latency-bound, not bandwidth-bound"},
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -428,8 +526,22 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def spawn(args) -> int:
+    """--gpus N > 1 without a torchrun environment: re-launch this script
+    under torch.distributed.run with N ranks on this node."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = _args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     if args.impl == "reference":
         run_reference(args)
     else:

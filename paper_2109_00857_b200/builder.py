@@ -439,6 +439,7 @@ class DeviceModel:
     def export_device(self):
         """Canonical COO on the device: (block_off, rows, cols, vals, rewards)."""
         torch = _torch()
+        self.check()   # a deferred build: census (nnz sizes the outputs), overflow, capacity
         dev = self.reward.device
         nb = self.n_actions * self.grid.nt
         scratch = torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev)

@@ -22,15 +22,27 @@ from .rollout import ensemble_rollout
 from .solver import value_iteration
 
 
+# RunConfig defaults of the reference (config.py:182-196): a run config that
+# omits a key builds the same actions and rewards as the reference pipeline
+RUN_DEFAULTS = {"objective": "time", "c_f": 1.0, "c_r": 1.0, "r_term": 100.0, "r_outbound": -1000.0,
+                "n_headings": 8, "n_speeds": 2, "f_max": 1.0, "epsilon": 1e-8, "max_iterations": None,
+                "subgrid_buffer": 1}
+
+
+def _get(cfg, key):
+    v = cfg.get(key)
+    return RUN_DEFAULTS[key] if v is None else v
+
+
 def _actions(cfg) -> ActionSpace:
-    return ActionSpace(n_headings=int(cfg.get("n_headings", 8)), n_speeds=int(cfg.get("n_speeds", 1)),
-                       f_max=float(cfg.get("f_max", 1.0)))
+    return ActionSpace(n_headings=int(_get(cfg, "n_headings")), n_speeds=int(_get(cfg, "n_speeds")),
+                       f_max=float(_get(cfg, "f_max")))
 
 
 def _rewards(cfg) -> RewardConfig:
-    return RewardConfig(objective=cfg.get("objective", "time"), c_f=float(cfg.get("c_f", 1.0)),
-                        c_r=float(cfg.get("c_r", 0.0)), r_term=float(cfg.get("r_term", 100.0)),
-                        r_outbound=float(cfg.get("r_outbound", -100.0)))
+    return RewardConfig(objective=_get(cfg, "objective"), c_f=float(_get(cfg, "c_f")),
+                        c_r=float(_get(cfg, "c_r")), r_term=float(_get(cfg, "r_term")),
+                        r_outbound=float(_get(cfg, "r_outbound")))
 
 
 def run_build(cfg) -> dict:
@@ -39,7 +51,7 @@ def run_build(cfg) -> dict:
     acts = _actions(cfg)
     ctx = StepContext(env, acts, _rewards(cfg), tuple(cfg["target"]))
     denv = ctx.device_env()
-    sub = compute_subgrid(env.field, acts, env.grid, buffer=int(cfg.get("subgrid_buffer", 1)), device_env=denv)
+    sub = compute_subgrid(env.field, acts, env.grid, buffer=int(_get(cfg, "subgrid_buffer")), device_env=denv)
     t0 = time.perf_counter()
     dm = build_device_model(denv, acts, ctx.rcfg, ctx.target, sub)
     elapsed = time.perf_counter() - t0
@@ -53,8 +65,8 @@ def run_solve(cfg) -> dict:
     """Model file -> policy file by value iteration (pipeline.py:123-136): the
     model's f32 probabilities / rewards widened to f64, as the reference reads them."""
     model = io.read_model(cfg["model"])
-    pv = value_iteration(model, SolverConfig(epsilon=float(cfg.get("epsilon", 1e-8)),
-                                             max_iterations=cfg.get("max_iterations")))
+    pv = value_iteration(model, SolverConfig(epsilon=float(_get(cfg, "epsilon")),
+                                             max_iterations=_get(cfg, "max_iterations")))
     io.write_policy(cfg["policy"], pv.values, pv.actions)
     return {"out": str(cfg["policy"]), "iterations_run": pv.iterations_run, "residual": pv.residual,
             "converged": pv.converged}
@@ -71,7 +83,7 @@ def run_rollout(cfg) -> dict:
     ens = ensemble_rollout(ctx, actions, start)
     io.write_trajectories_csv(cfg["trajectories"], ens)
     summary = ens.summary()
-    summary.update({"objective": cfg.get("objective", "time"), "start": list(start), "target": list(target),
+    summary.update({"objective": _get(cfg, "objective"), "start": list(start), "target": list(target),
                     "policy_value_at_start": float(values[env.grid.state_index(start[0], start[1], 0)]),
                     "trajectories_out": str(cfg["trajectories"])})
     spath = cfg.get("summary") or (str(cfg["trajectories"]) + ".summary.json")

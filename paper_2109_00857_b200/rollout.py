@@ -129,9 +129,21 @@ def _trajectories(ctx, policy, start, reals) -> list:
     si, sj = int(start[0]), int(start[1])
     if not (0 <= si < grid.nx and 0 <= sj < grid.ny):
         raise ContractViolation(f"start cell {tuple(start)} outside grid")
-    pol_max = int(policy.max()) if hasattr(policy, "max") and np.shape(policy)[0] else 0
-    if pol_max >= ctx.act_vecs.shape[0]:
-        raise ContractViolation(f"policy action {pol_max} out of range")
+    n_act = ctx.act_vecs.shape[0]
+    if np.shape(policy)[0]:
+        p_min = int(policy.min()) if hasattr(policy, "min") else int(min(policy))
+        p_max = int(policy.max()) if hasattr(policy, "max") else int(max(policy))
+        if p_min < 0 or p_max >= n_act:
+            bad = p_max if p_max >= n_act else p_min
+            raise ContractViolation(f"policy action {bad} out of range")
+    # realization indices follow numpy indexing of coeffs[t, r] (rollout.py:
+    # reconstruct_timeslice): negatives wrap, anything else out of range raises
+    n_real = int(ctx.env.field.coeffs.shape[1])
+    dev_reals = []
+    for r in reals:
+        if not -n_real <= r < n_real:
+            raise IndexError(f"index {r} is out of bounds for axis 1 with size {n_real}")
+        dev_reals.append(r + n_real if r < 0 else r)
     centers = grid.cell_centers()
     cell0 = sj * grid.nx + si
     if bool(np.asarray(ctx.env.obstacles.mask)[0].reshape(-1)[cell0]):
@@ -144,7 +156,7 @@ def _trajectories(ctx, policy, start, reals) -> list:
                 for r in reals]
     if not reals:
         return []
-    n_rows, fin, rc, ra, rca, rr, rcum = rollout_device(ctx, policy, (si, sj), reals)
+    n_rows, fin, rc, ra, rca, rr, rcum = rollout_device(ctx, policy, (si, sj), dev_reals)
     xs, ys = centers[:, 0].tolist(), centers[:, 1].tolist()
     trajs = []
     for k, r in enumerate(reals):

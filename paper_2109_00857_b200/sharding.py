@@ -67,6 +67,18 @@ def all_reduce_max(tensor, group=None) -> None:
         dist.all_reduce(tensor, op=dist.ReduceOp.MAX, group=group)
 
 
+def all_reduce_sum(tensor, group=None) -> None:
+    """In-place SUM all-reduce (device buffers under NCCL)."""
+    import torch.distributed as dist
+
+    if host_staged(tensor, group):
+        h = tensor.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        tensor.copy_(h)
+    else:
+        dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
+
+
 def exchange_layer(values, t: int, nx: int, ny: int, hy: int, group=None) -> int:
     """Exchange halo rows of layer t of the flat value vector in place.
     Returns the number of bytes this rank sent."""

@@ -82,3 +82,42 @@ def test_rollout_contract_errors():
         ensemble_rollout(ctx, pol[:-1], (0, 0) if tuple(target) != (0, 0) else (1, 0))
     with pytest.raises(fm.ContractViolation):
         ensemble_rollout(ctx, pol, tuple(target))
+
+
+def test_rollout_negative_realizations_wrap_like_numpy():
+    """coeffs[t, r] with r < 0 wraps (numpy indexing in the reference's
+    rollout): trajectory -1 follows realization N_rv - 1 and keeps -1 as
+    its label."""
+    env, acts, rcfg, target = make_random_env(7001)
+    ctx = fm.StepContext(env, acts, rcfg, target)
+    pv = fm.value_iteration(fm.build_model(ctx, fm.compute_subgrid(env.field, acts, env.grid)))
+    start = (0, 0) if tuple(target) != (0, 0) else (1, 0)
+    n_real = env.field.coeffs.shape[1]
+    a = simulate_trajectory(ctx, pv.actions, start, -1)
+    b = simulate_trajectory(ctx, pv.actions, start, n_real - 1)
+    assert a.realization == -1 and b.realization == n_real - 1
+    assert a.rows == b.rows and a.status == b.status and a.cum_reward == b.cum_reward
+
+
+def test_export_of_a_deferred_build_runs_the_check_first():
+    """to_sparse_model / value_iteration on a model built with defer_check
+    (and an entry buffer too small for it) finish the census / capacity
+    retry before sizing the export: same model as the checked build."""
+    env, acts, rcfg, target = make_random_env(7004)
+    ctx = fm.StepContext(env, acts, rcfg, target)
+    sub = fm.compute_subgrid(env.field, acts, env.grid)
+    denv = ctx.device_env()
+    ref = fm.build_device_model(denv, acts, rcfg, target, sub).to_sparse_model()
+    dm = fm.build_device_model(denv, acts, rcfg, target, sub, defer_check=True, capacity_hint=1)
+    sm = dm.to_sparse_model()
+    assert sm.nnz_total() == ref.nnz_total()
+    for a in range(acts.n_actions):
+        for t in range(env.grid.nt):
+            x, y = sm.blocks[a][t], ref.blocks[a][t]
+            assert np.array_equal(x.rows, y.rows) and np.array_equal(x.cols, y.cols)
+            assert x.vals.tobytes() == y.vals.tobytes()
+    assert sm.rewards.tobytes() == ref.rewards.tobytes()
+    dm2 = fm.build_device_model(denv, acts, rcfg, target, sub, defer_check=True, capacity_hint=1)
+    pv = fm.value_iteration(dm2)
+    pv_ref = fm.value_iteration(ref)
+    assert pv.values.tobytes() == pv_ref.values.tobytes()
