@@ -126,6 +126,12 @@ typedef struct {
      *    lean path floors with one round-down add instead of F2I. */
     const fm_action *h_actions;
     double vmax_x, vmax_y;
+    /* Optional (NULL = none): the velocity envelope of fm_velocity_scan
+     * covering the build's slabs x strip.  With it (and the two enablers
+     * above) lean cells are built per (cell, realization) instead of per
+     * (cell, action, realization): each realization is binned once against
+     * the action set's landing thresholds; the counts are unchanged. */
+    const int32_t *envelope;
 } fm_build_args;
 
 /* Sub-grid overflow report (message of model_builder.py:433-438). */
@@ -153,6 +159,15 @@ int32_t fm_velocity_max_rows(fm_grid grid, fm_env env, int32_t j0, int32_t j1,
  * maxima over slabs are the full scan's). */
 int32_t fm_velocity_max_slab(fm_grid grid, fm_env env, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
                              double *d_out2, void *stream);
+/* fm_velocity_max_slab plus, when d_envelope is not NULL, the per-(t, cell)
+ * velocity envelope of the scanned cells: d_envelope is int32 [nt][N_c][4]
+ * (x_lo, x_hi, y_lo, y_hi as order-preserving encodings of f32 bounds that
+ * contain every reconstructed v(t, r, cell) of environment.py:293-297).
+ * fm_build bins the realizations of a cell against it (fm_build_args.
+ * envelope).  Same reference function as above (model_builder.py:392-396):
+ * the envelope is a by-product of the scan. */
+int32_t fm_velocity_scan(fm_grid grid, fm_env env, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
+                         double *d_out2, int32_t *d_envelope, void *stream);
 
 /* Segmented max-abs used by velocity_bound (environment.py:404-419):
  * d_out[s] = max_k |src[(s / inner) * outer_stride + (s % inner) * inner_stride

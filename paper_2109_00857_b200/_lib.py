@@ -91,7 +91,8 @@ class FmBuildArgs(C.Structure):
                 ("mask_sat", C.c_void_p),
                 ("t0", C.c_int32), ("t1", C.c_int32), ("j0", C.c_int32), ("j1", C.c_int32),
                 ("viol_flags", C.c_void_p), ("task_counter", C.c_void_p), ("d_gate_r", C.c_void_p),
-                ("h_actions", C.c_void_p), ("vmax_x", C.c_double), ("vmax_y", C.c_double)]
+                ("h_actions", C.c_void_p), ("vmax_x", C.c_double), ("vmax_y", C.c_double),
+                ("envelope", C.c_void_p)]
 
 
 class FmViolation(C.Structure):
@@ -124,6 +125,8 @@ SIGNATURES = {
     "fm_velocity_max_rows": (C.c_int32, [FmGrid, FmEnv, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "fm_velocity_max_slab": (C.c_int32, [FmGrid, FmEnv, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                          C.c_void_p]),
+    "fm_velocity_scan": (C.c_int32, [FmGrid, FmEnv, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                     C.c_void_p, C.c_void_p]),
     "fm_maxabs_segments": (C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                        C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
     "fm_mask_sat": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),

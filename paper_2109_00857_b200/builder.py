@@ -53,6 +53,21 @@ class DeviceEnv:
     _vmax: tuple | None = None
     _acts: dict = field(default_factory=dict)
     _scan: tuple | None = None   # (device maxima, j_range) of a scan done during upload
+    envelope: object = None      # int32 [nt][N_c][4] per-cell velocity envelope (fm_velocity_scan)
+    _env_rows: tuple | None = None   # rows [j0, j1) whose envelope is current (all layers)
+
+    def _envelope_buf(self):
+        if self.envelope is None:
+            torch = _torch()
+            g = self.grid
+            self.envelope = torch.empty((g.nt, g.nx * g.ny, 4), dtype=torch.int32, device=self.mean.device)
+        return self.envelope
+
+    def envelope_for(self, j0: int, j1: int):
+        """Device pointer of the envelope if it covers rows [j0, j1), else None."""
+        if self._env_rows is not None and self._env_rows[0] <= j0 and j1 <= self._env_rows[1]:
+            return self.envelope.data_ptr()
+        return None
 
     def action_table(self, recs: np.ndarray):
         """Device copy of an action-record table (cached by content)."""
@@ -129,6 +144,7 @@ class DeviceEnv:
         nt = grid.nt
         bounds = [nt * i // max(1, min(slabs, nt)) for i in range(max(1, min(slabs, nt)) + 1)]
         lib = _lib.load()
+        env_ptr = de._envelope_buf().data_ptr()
         for t0, t1 in zip(bounds[:-1], bounds[1:]):
             with torch.cuda.stream(copy):
                 dst["mean"][t0:t1].copy_(src["mean"][t0:t1], non_blocking=True)
@@ -138,8 +154,8 @@ class DeviceEnv:
                 ev = torch.cuda.Event()
                 ev.record(copy)
             main.wait_event(ev)
-            _lib.check(lib.fm_velocity_max_slab(de.fm_grid(), de.fm_env(), int(t0), int(t1), int(j0), int(j1),
-                                                out.data_ptr(), _lib.stream_ptr(main)), "fm_velocity_max_slab")
+            _lib.check(lib.fm_velocity_scan(de.fm_grid(), de.fm_env(), int(t0), int(t1), int(j0), int(j1),
+                                            out.data_ptr(), env_ptr, _lib.stream_ptr(main)), "fm_velocity_scan")
         with torch.cuda.stream(copy):
             dst["g"].copy_(src["g"], non_blocking=True)
             dst["mask"].copy_(src["mask"], non_blocking=True)
@@ -148,6 +164,7 @@ class DeviceEnv:
             v.record_stream(copy)
         de._make_sat()
         de._scan = (out, tuple(j_range) if j_range is not None else None)
+        de._env_rows = (int(j0), int(j1))
         return de
 
     def _make_sat(self):
@@ -172,6 +189,7 @@ class DeviceEnv:
         self._vmax = None
         self._vbound = {}
         self._scan = None
+        self._env_rows = None
 
     def velocity_max(self, j_range: tuple | None = None, group=None) -> tuple:
         """Exact max |v_x|, |v_y| over (t, r, cell) -- compute_subgrid's scan.
@@ -193,13 +211,13 @@ class DeviceEnv:
         if self._vmax is None:
             torch = _torch()
             out = torch.zeros(2, dtype=torch.float64, device=self.mean.device)
-            if j_range is None:
-                _lib.check(_lib.load().fm_velocity_max(self.fm_grid(), self.fm_env(), out.data_ptr(),
-                                                       _lib.stream_ptr()), "fm_velocity_max")
-            else:
-                _lib.check(_lib.load().fm_velocity_max_rows(self.fm_grid(), self.fm_env(), int(j_range[0]),
-                                                            int(j_range[1]), out.data_ptr(), _lib.stream_ptr()),
-                           "fm_velocity_max_rows")
+            # the scan also writes the per-cell envelope the build bins against
+            r0, r1 = (0, self.grid.ny) if j_range is None else (int(j_range[0]), int(j_range[1]))
+            _lib.check(_lib.load().fm_velocity_scan(self.fm_grid(), self.fm_env(), 0, self.grid.nt, r0, r1,
+                                                    out.data_ptr(), self._envelope_buf().data_ptr(),
+                                                    _lib.stream_ptr()), "fm_velocity_scan")
+            self._env_rows = (r0, r1)
+            if j_range is not None:
                 if group is not None or _dist_world() > 1:
                     from .sharding import all_reduce_max
                     all_reduce_max(out, group)   # non-negative: max of maxima
@@ -540,7 +558,8 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     recs = np.ascontiguousarray(recs)
     args = _lib.FmBuildArgs(denv.fm_grid(), denv.fm_env(), rw, d_act.data_ptr(), na, hx, hy, 0, 0,
                             denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr(),
-                            d_gate.data_ptr(), recs.ctypes.data if lean else None, vmx, vmy)
+                            d_gate.data_ptr(), recs.ctypes.data if lean else None, vmx, vmy,
+                            denv.envelope_for(j0, j1) if lean else None)
     if entries is None:
         entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
     dm = DeviceModel(grid=grid, n_actions=na, n_real=denv.n_real, subgrid=subgrid,

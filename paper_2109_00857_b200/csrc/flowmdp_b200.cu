@@ -12,7 +12,10 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
+#include <cstring>
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -94,7 +97,9 @@ static int sm_count()
 
 // Development counters (-DFM_STATS): [0] rare transitions, [1] exact
 // segment samplings, [2] segment samples, [3] transitions in obstacle warps,
-// [4] transitions in lean warps.  Not part of the ABI header.
+// [4] transitions in lean warps (per transition), [5] binned tasks, [6]
+// realizations of binned tasks taking the exact path, [7] lean tasks of a
+// bin launch that did not fit the bins.  Not part of the ABI header.
 #ifdef FM_STATS
 __device__ unsigned long long g_fm_stats[8];
 #define FM_STAT(i, n) atomicAdd(&g_fm_stats[i], (unsigned long long)(n))
@@ -193,9 +198,43 @@ static constexpr int kVmaxCells = 2;
 #endif
 static constexpr int kVmaxStep = FM_VMAX_STEP;   // realizations per step
 
+// Per-(t, cell) velocity envelope (the build's bin ranges): int4 of
+// order-preserving encodings of f32 (x_lo, x_hi, y_lo, y_hi), each already
+// widened by the cell's error bound so it contains every exact f64 value.
+__device__ __forceinline__ int f32_ord(float f)
+{
+    const int b = __float_as_int(f);
+    return b >= 0 ? b : b ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float ord_f32(int e) { return __int_as_float(e >= 0 ? e : e ^ 0x7FFFFFFF); }
+
+__device__ __forceinline__ void store_envelope(int4 *vr, size_t idx, float xlo, float xhi, float ylo, float yhi,
+                                               bool direct)
+{
+    const int4 e = make_int4(f32_ord(xlo), f32_ord(xhi), f32_ord(ylo), f32_ord(yhi));
+    if (direct) {
+        vr[idx] = e;
+    } else {
+        int *p = reinterpret_cast<int *>(vr + idx);
+        atomicMin(p, e.x);
+        atomicMax(p + 1, e.y);
+        atomicMin(p + 2, e.z);
+        atomicMax(p + 3, e.w);
+    }
+}
+
+__global__ void k_envelope_init(int4 *vr, int nc, int t0, int nts, int cell0, int ncell)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)nts * ncell) return;
+    const int t = t0 + (int)(i / ncell), c = cell0 + (int)(i % ncell);
+    const int pinf = 0x7f800000, ninf = f32_ord(__int_as_float(0xff800000));
+    vr[(size_t)t * nc + c] = make_int4(pinf, ninf, pinf, ninf);
+}
+
 template <int NMX>
 __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int cell0, int ncell, int r_per_block,
-                                               const double *cmax, double *out2)
+                                               const double *cmax, double *out2, int4 *vrange)
 {
     __shared__ float cs[kVmaxChunk][NMX];
     const int nc = G.nx * G.ny;
@@ -240,6 +279,12 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
         dely[q] = Ty * kRel + kAbs;
     }
     double ex = 0.0, ey = 0.0;   // running exact maxima (shared by this thread's cells)
+    float2 vlo[kVmaxCells], vhi[kVmaxCells];   // envelope of the f32 reconstructions
+#pragma unroll
+    for (int q = 0; q < kVmaxCells; ++q) {
+        vlo[q] = make_float2(__int_as_float(0x7f800000), __int_as_float(0x7f800000));
+        vhi[q] = make_float2(__int_as_float(0xff800000), __int_as_float(0xff800000));
+    }
     float thx[kVmaxCells], thy[kVmaxCells];
 #pragma unroll
     for (int q = 0; q < kVmaxCells; ++q) {
@@ -278,6 +323,17 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
                     for (int q = 0; q < kVmaxCells; ++q) v[j][q] = ffma2_bcast(cj, d32[q][m], v[j][q]);
                 }
             }
+            if (vrange) {
+#pragma unroll
+                for (int j = 0; j < kVmaxStep; ++j)
+#pragma unroll
+                    for (int q = 0; q < kVmaxCells; ++q) {
+                        vlo[q].x = fminf(vlo[q].x, v[j][q].x);
+                        vhi[q].x = fmaxf(vhi[q].x, v[j][q].x);
+                        vlo[q].y = fminf(vlo[q].y, v[j][q].y);
+                        vhi[q].y = fmaxf(vhi[q].y, v[j][q].y);
+                    }
+            }
             // !(|v| < th) also routes NaN / inf to the exact path
             bool hit = false;
 #pragma unroll
@@ -311,6 +367,16 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
             }
         }
     }
+    if (vrange) {
+        // widened by the cell's bound delta >= |v32 - v64| (rounded outwards)
+#pragma unroll
+        for (int q = 0; q < kVmaxCells; ++q)
+            if (ok[q])
+                store_envelope(vrange, (size_t)t * nc + cell[q], __fsub_rd(vlo[q].x, __double2float_ru(delx[q])),
+                               __fadd_ru(vhi[q].x, __double2float_ru(delx[q])),
+                               __fsub_rd(vlo[q].y, __double2float_ru(dely[q])),
+                               __fadd_ru(vhi[q].y, __double2float_ru(dely[q])), gridDim.z == 1);
+    }
     // non-negative doubles (and +NaN, above +inf) order like their bit patterns
     unsigned long long bx = (unsigned long long)__double_as_longlong(ex),
                        by = (unsigned long long)__double_as_longlong(ey);
@@ -337,7 +403,7 @@ __global__ void k_maxabs_seg(const double *src, int64_t seg_len, int64_t elem_st
 // realization's sum still runs in mode order (environment.py:293-297).
 template <int RB>
 __global__ void __launch_bounds__(256) k_vmax_f64(fm_grid G, fm_env E, int t0, int cell0, int ncell,
-                                                   int r_per_block, double *out2)
+                                                   int r_per_block, double *out2, int4 *vrange)
 {
     const int nc = G.nx * G.ny;
     const int t = t0 + blockIdx.y;
@@ -348,6 +414,7 @@ __global__ void __launch_bounds__(256) k_vmax_f64(fm_grid G, fm_env E, int t0, i
     const int r_lo = blockIdx.z * r_per_block;
     const int r_hi = min(E.n_real, r_lo + r_per_block);
     double ex = 0.0, ey = 0.0;
+    double lx = INFINITY, hx = -INFINITY, ly = INFINITY, hy = -INFINITY;   // exact envelope
     if (ok) {
         const double2 mu = *reinterpret_cast<const double2 *>(E.mean + ((size_t)t * nc + c) * 2);
         for (int r0 = r_lo; r0 < r_hi; r0 += RB) {
@@ -369,8 +436,15 @@ __global__ void __launch_bounds__(256) k_vmax_f64(fm_grid G, fm_env E, int t0, i
                 const double ax = fabs(vx[q]), ay = fabs(vy[q]);
                 ex = (ax != ax || ax > ex) ? ax : ex;   // NaN sticks
                 ey = (ay != ay || ay > ey) ? ay : ey;
+                lx = fmin(lx, vx[q]);
+                hx = fmax(hx, vx[q]);
+                ly = fmin(ly, vy[q]);
+                hy = fmax(hy, vy[q]);
             }
         }
+        if (vrange)
+            store_envelope(vrange, (size_t)t * nc + c, __double2float_rd(lx), __double2float_ru(hx),
+                           __double2float_rd(ly), __double2float_ru(hy), gridDim.z == 1);
     }
     unsigned long long bx = (unsigned long long)__double_as_longlong(ex),
                        by = (unsigned long long)__double_as_longlong(ey);
@@ -391,13 +465,22 @@ extern "C" int32_t fm_velocity_max(fm_grid G, fm_env E, double *d_out2, void *st
     return fm_velocity_max_rows(G, E, 0, G.ny, d_out2, stream);
 }
 
+extern "C" int32_t fm_velocity_scan(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
+                                    double *d_out2, int32_t *d_envelope, void *stream);
+
+extern "C" int32_t fm_velocity_max_slab(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
+                                        double *d_out2, void *stream)
+{
+    return fm_velocity_scan(G, E, t0, t1, j0, j1, d_out2, nullptr, stream);
+}
+
 extern "C" int32_t fm_velocity_max_rows(fm_grid G, fm_env E, int32_t j0, int32_t j1, double *d_out2, void *stream)
 {
     return fm_velocity_max_slab(G, E, 0, G.nt, j0, j1, d_out2, stream);
 }
 
-extern "C" int32_t fm_velocity_max_slab(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
-                                        double *d_out2, void *stream)
+extern "C" int32_t fm_velocity_scan(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
+                                    double *d_out2, int32_t *d_envelope, void *stream)
 {
     if (G.nx < 1 || G.ny < 1 || G.nt < 1 || E.n_real < 1 || E.n_modes < 0)
         return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims");
@@ -408,13 +491,20 @@ extern "C" int32_t fm_velocity_max_slab(fm_grid G, fm_env E, int32_t t0, int32_t
     const int nc = (j1 - j0) * G.nx;   // cells scanned
     const int nm = E.n_modes;
     const int nts = t1 - t0;           // layers scanned
+    int4 *vr = reinterpret_cast<int4 *>(d_envelope);
     if (nm > 16) {
         const int bxf = (nc + 255) / 256;
         const long long basef = (long long)bxf * nts, want = 4LL * sm_count();
         int rpb = E.n_real;
         if (basef < want) rpb = (int)((E.n_real + (want + basef - 1) / basef - 1) / ((want + basef - 1) / basef));
         if (rpb < 1) rpb = 1;
-        k_vmax_f64<8><<<dim3(bxf, nts, (E.n_real + rpb - 1) / rpb), 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, d_out2);
+        const int nz = (E.n_real + rpb - 1) / rpb;
+        if (vr && nz > 1) {
+            k_envelope_init<<<(unsigned)(((long long)nts * nc + 255) / 256), 256, 0, s>>>(vr, G.nx * G.ny, t0, nts,
+                                                                                          j0 * G.nx, nc);
+            FM_CK_LAUNCH("k_envelope_init");
+        }
+        k_vmax_f64<8><<<dim3(bxf, nts, nz), 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, d_out2, vr);
         FM_CK_LAUNCH("k_vmax_f64");
         return FM_OK;
     }
@@ -436,12 +526,17 @@ extern "C" int32_t fm_velocity_max_slab(fm_grid G, fm_env E, int32_t t0, int32_t
         rpb = ((rpb + kVmaxChunk - 1) / kVmaxChunk) * kVmaxChunk;
     }
     dim3 grid(bx, nts, (E.n_real + rpb - 1) / rpb);
+    if (vr && grid.z > 1) {
+        k_envelope_init<<<(unsigned)(((long long)nts * nc + 255) / 256), 256, 0, s>>>(vr, G.nx * G.ny, t0, nts,
+                                                                                      j0 * G.nx, nc);
+        FM_CK_LAUNCH("k_envelope_init");
+    }
     if (nm <= 4)
-        k_vmax<4><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2);
+        k_vmax<4><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2, vr);
     else if (nm <= 8)
-        k_vmax<8><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2);
+        k_vmax<8><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2, vr);
     else
-        k_vmax<16><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2);
+        k_vmax<16><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2, vr);
     FM_CK_LAUNCH("k_vmax");
     FM_CK(cudaFreeAsync(cmax, s));
     return FM_OK;
@@ -533,6 +628,36 @@ enum : int {
 };
 enum : int { RF_DEAD = 1, RF_TERMINAL = 2, RF_GATE = 4, RF_LANDWIN = 8, RF_SEGWIN = 16 };
 
+// Per-(cell, realization) binning of lean tasks (F_PROVEN | F_CNT).
+//
+// With p = dx / dt and z = v / p, the landing of action a from cell column
+// ci is ci + floor(z + c_a), c_a = 0.5 + a_x / p (model_builder.py:331-335
+// in real arithmetic; x0 = origin + (ci + 0.5) dx, environment.py:99-100).
+// Writing c_a = gamma_a + beta_a (integer + fraction), the displacement is
+// gamma_a + floor(z) + [frac(z) >= theta_a], theta_a = 1 - beta_a: every
+// action's landing is a step function of z whose steps sit at n + theta_a.
+// The union of the theta_a (clustered, see bin_axis) cuts each unit of z
+// into K + 1 sub-bins; a realization's bin (n, sub) in x and in y fixes its
+// landing for EVERY action, so one 2-D histogram of bins per cell replaces
+// the per-(cell, action, realization) work, and each row's counts are
+// rectangle sums of it.  Exactness: z is computed in f32 with a rigorous
+// error bound; a realization closer than the zone half-width to any step
+// (or with any doubt) takes the exact f64 path of the reference instead
+// (bin_drain), so the counts equal the reference's bit for bit.
+static constexpr int kBinNS = 128;    // buckets per unit interval of frac(z)
+static constexpr int kBinMaxA = 64;   // actions with bin parameters
+static constexpr int kBinRing = 8;    // coefficient chunks in flight (32 realizations each)
+static constexpr int kBinQ = 128;     // deferred exact realizations per warp
+struct BinEnt {
+    // the zone intersecting the bucket: frac in [lo, hi] -> exact path; the
+    // low 6 mantissa bits of lo hold kb + 1, kb = the sub-bin below the zone
+    // (or of the whole bucket): lo is rounded down first, so the zone only widens
+    float lo, hi;
+};
+struct BinAct {
+    int gx, rx, gy, ry;   // gamma and cluster index (0 = always, K+1 = never) per axis
+};
+
 struct BuildK {
     // grid
     int nx, ny, nt, nc;
@@ -573,6 +698,23 @@ struct BuildK {
     uint32_t *viol;
     unsigned int *task_counter;
     uint16_t *ghist;   // F_GHIST: [resident warp][nslot + 1][32]
+    // ---- per-(cell, realization) binning of lean tasks (see bin_task) ----
+    int bin_ok;                 // the launch has bin tables (PART 1 lean tasks use them)
+    int bin_k1x, bin_k1y;       // sub-bins per unit of z = v / p, per axis (clusters + 1)
+    int bin_p1;                 // p = dx / dt == 1 (z = v)
+    float bin_ip;               // f32(1 / p)
+    double bin_p;               // p
+    double bin_dzone;           // zone half-width in z units (per-cell error must not exceed it)
+    double bin_eps;             // allowance for the reference's own landing roundings (z units)
+    int bin_words;              // u32 bin counters per warp
+    int off_block;              // block-shared bytes before the warps' regions (bin tables)
+    int off_bins, off_bdense, off_bq;   // per-warp regions of the bin path (union with the legacy ones):
+                                        // counters | coefficient ring, later the dense histogram | queue
+    const float *coef32;        // [t - t0][nr][8] f32 coefficients (zero padded), per launch
+    const double *cmax;         // [t - t0][nm] max_r |coeff[t, r, m]|
+    const int4 *envelope;       // [nt][nc] per-cell velocity envelope (fm_velocity_scan) or null
+    BinEnt tab[2 * (kBinNS + 1)];   // bucket tables, x then y (entry NS: frac == 1)
+    BinAct bact[kBinMaxA];      // per action: (gamma_x, cluster r_x, gamma_y, r_y)
 };
 
 // fl(q / n) for 0 <= q <= n <= kFracMaxN at g_frac[n (n + 1) / 2 + q]: the
@@ -1333,6 +1475,398 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
     }
 }
 
+// ---- per-(cell, realization) binning (lean tasks, F_PROVEN | F_CNT) --------
+
+__device__ __forceinline__ unsigned long long f2_bits(float2 a) { return *reinterpret_cast<unsigned long long *>(&a); }
+__device__ __forceinline__ float2 f2_from(unsigned long long r) { return *reinterpret_cast<float2 *>(&r); }
+__device__ __forceinline__ float2 f2_add_rm(float2 a, float2 b)
+{
+    unsigned long long r;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(r);
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b)
+{
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(r);
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b)
+{
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(r);
+}
+__device__ __forceinline__ float2 f2_fma_rm(float2 a, float2 b, float2 c)
+{
+    unsigned long long r;
+    asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+    return f2_from(r);
+}
+__device__ __forceinline__ void cp_async_wait_ring() { asm volatile("cp.async.wait_group %0;\n" ::"n"(kBinRing - 1) : "memory"); }
+
+// One cell of a bin task: f32 reconstruction inputs and the bin box.
+struct BinCell {
+    float2 mu;
+    float2 md[8];
+    int offx, offy;   // n_lo * (K + 1) per axis: bin = n * (K + 1) + sub - off
+    int bx, by;       // bins per axis
+    int base;         // first u32 counter of this cell in the warp's bin region
+};
+
+// Setup of cell c at layer t: error bound, envelope, bin box.  False when
+// the cell cannot be binned (its f32 error exceeds the zone half-width, or
+// its box is too large); the task then takes the per-transition path.
+__device__ __forceinline__ bool bin_setup(const BuildK &K, int t, int c, BinCell &B, int &words)
+{
+    const size_t cell = (size_t)t * K.nc + c;
+    const double2 mu = *reinterpret_cast<const double2 *>(K.mean + cell * 2);
+    const double *cm = K.cmax + (size_t)(t - K.t0) * K.nm;
+    double Px = 0.0, Py = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        B.md[m] = make_float2(0.f, 0.f);
+        if (m < K.nm) {
+            const double2 md = *reinterpret_cast<const double2 *>(K.modes + (((size_t)m * K.nt + t) * K.nc + c) * 2);
+            B.md[m] = make_float2((float)md.x, (float)md.y);
+            const double w = cm[m];
+            Px += fabs(md.x) * w;
+            Py += fabs(md.y) * w;
+        }
+    }
+    B.mu = make_float2((float)mu.x, (float)mu.y);
+    const double Tx = fabs(mu.x) + Px, Ty = fabs(mu.y) + Py;
+    // |v32 - v64| <= delta (the k_vmax bound: f32 inputs, FMA chain, and the
+    // reference's own f64 rounding); then z = v32 * f32(1/p), floor/frac in
+    // f32: 2^-21 (|z| + 1) covers the scaling and the frac subtraction
+    const double kRel = (2.0 * K.nm + 8.0) * 0x1p-24 * 1.001, kAbs = (K.nm + 2.0) * 0x1p-140;
+    const double dlx = Tx * kRel + kAbs, dly = Ty * kRel + kAbs;
+    const double ip = 1.0 / K.bin_p;
+    const double Dx = dlx * ip + 0x1p-21 * (Tx * ip + 1.0) + K.bin_eps;
+    const double Dy = dly * ip + 0x1p-21 * (Ty * ip + 1.0) + K.bin_eps;
+    if (!(Dx <= K.bin_dzone && Dy <= K.bin_dzone)) return false;
+    double xlo, xhi, ylo, yhi;
+    if (K.envelope) {   // widened by delta in the scan: contains v64 and v32
+        const int4 e = K.envelope[cell];
+        xlo = ord_f32(e.x); xhi = ord_f32(e.y); ylo = ord_f32(e.z); yhi = ord_f32(e.w);
+        xlo -= dlx; xhi += dlx; ylo -= dly; yhi += dly;
+    } else {            // triangle bound around the mean
+        xlo = mu.x - Px - 2.0 * dlx; xhi = mu.x + Px + 2.0 * dlx;
+        ylo = mu.y - Py - 2.0 * dly; yhi = mu.y + Py + 2.0 * dly;
+    }
+    const double zxl = xlo * ip - Dx, zxh = xhi * ip + Dx, zyl = ylo * ip - Dy, zyh = yhi * ip + Dy;
+    if (!(fabs(zxl) < 0x1p20 && fabs(zxh) < 0x1p20 && fabs(zyl) < 0x1p20 && fabs(zyh) < 0x1p20)) return false;
+    const int nxl = (int)floor(zxl), nxh = (int)floor(zxh), nyl = (int)floor(zyl), nyh = (int)floor(zyh);
+    B.bx = (nxh - nxl + 1) * K.bin_k1x;
+    B.by = (nyh - nyl + 1) * K.bin_k1y;
+    B.offx = nxl * K.bin_k1x;
+    B.offy = nyl * K.bin_k1y;
+    words = B.bx * B.by;
+    return words <= K.bin_words;
+}
+
+// Exact f64 velocity of (t, r, cell c) in the reference's order
+// (environment.py:293-297: v = mean; v = v + c_m * mode_m, ascending m).
+__device__ __forceinline__ double2 exact_velocity(const BuildK &K, int t, int r, int c)
+{
+    const double2 mu = *reinterpret_cast<const double2 *>(K.mean + ((size_t)t * K.nc + c) * 2);
+    double vx = mu.x, vy = mu.y;
+    const double *cf = K.coeffs + ((size_t)t * K.nr + r) * K.nm;
+    for (int m = 0; m < K.nm; ++m) {
+        const double2 md = *reinterpret_cast<const double2 *>(K.modes + (((size_t)m * K.nt + t) * K.nc + c) * 2);
+        const double k = __ldg(cf + m);
+        vx = DADD(vx, DMUL(k, md.x));
+        vy = DADD(vy, DMUL(k, md.y));
+    }
+    return make_double2(vx, vy);
+}
+
+// Deferred realizations (within a zone, or out of the box): the exact f64
+// velocity, then every row of its cell takes the reference's transition
+// (lean_transition, as the per-transition path) into the dense histogram.
+// Items are (cell slot << 16 | r); the last n <= 32 are processed.
+template <int FLAGS>
+__device__ __forceinline__ int bin_drain(const BuildK &K, const uint32_t *bq, int qn, int t, int grp,
+                                         const RowC &Rf, uint16_t *h16q, unsigned hs_word, int outq, bool row_ok,
+                                         int cs_row, unsigned half_one)
+{
+    const int lane = threadIdx.x & 31;
+    const int n = qn < 32 ? qn : 32, first = qn - n;
+    if (lane == 0) FM_STAT(6, n);
+    double2 v = make_double2(0.0, 0.0);
+    int cs = -1;
+    if (lane < n) {
+        const uint32_t it = bq[first + lane];
+        cs = (int)(it >> 16);
+        v = exact_velocity(K, t, (int)(it & 0xFFFFu), K.cell0 + grp * K.CW + cs);
+    }
+    for (int e = 0; e < n; ++e) {
+        const double vx = __shfl_sync(kFull, v.x, e), vy = __shfl_sync(kFull, v.y, e);
+        const int ce = __shfl_sync(kFull, cs, e);
+        if (row_ok && cs_row == ce) {
+            double w;
+            const int q = lean_transition<FLAGS, false>(K, Rf, make_double2(vx, vy), nullptr, outq, w);
+            hist_inc(h16q, hs_word, q, half_one);
+        }
+    }
+    __syncwarp();
+    return first;
+}
+
+// The realization loop of one bin task over NC (1 or 2) cells: f32
+// reconstruction, bin, one shared-memory increment per (cell, realization);
+// realizations with any doubt are queued for the exact path.  Coefficients
+// stream through a per-warp ring of 32-realization chunks (cp.async, kBinRing
+// chunks in flight), two chunks per iteration.  Returns the queue length, or
+// -1 when the queue overflowed (the task then takes the per-transition path).
+template <int NC>
+__device__ __forceinline__ int bin_loop(const BuildK &K, const BinCell *B, int p, int t, const BinEnt *tab_s,
+                                        unsigned bins_s, unsigned ring_s, uint32_t *bq)
+{
+    const int lane = threadIdx.x & 31, nr = K.nr;
+    const int nch = (nr + 31) >> 5;
+    const float2 ip2 = make_float2(K.bin_ip, K.bin_ip);
+    const float2 M2 = make_float2(12582912.0f, 12582912.0f);   // 1.5 * 2^23: floor by a round-down add
+    const float2 NS2 = make_float2((float)kBinNS, (float)kBinNS);
+    const unsigned tabx_s = (unsigned)__cvta_generic_to_shared(tab_s) - 0x4B400000u * 8u;   // bucket bits -> entry
+    const unsigned taby_s = tabx_s + (kBinNS + 1) * 8u;
+    const int k1x = K.bin_k1x, k1y = K.bin_k1y;
+    // bin = (bits(M + floor z) - bits(M)) * k1 + kb - off: constants folded
+    unsigned cx[NC], cy[NC];   // modulo 2^32: the products with the bias bits wrap and cancel
+    int bxn[NC], byn[NC];
+    unsigned bb[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        cx[q] = 0u - 0x4B400000u * (unsigned)k1x - (unsigned)B[q].offx;
+        cy[q] = 0u - 0x4B400000u * (unsigned)k1y - (unsigned)B[q].offy;
+        bxn[q] = B[q].bx;
+        byn[q] = B[q].by;
+        bb[q] = bins_s + 4u * (unsigned)B[q].base;
+    }
+    const char *gsrc = reinterpret_cast<const char *>(K.coef32 + (size_t)(t - K.t0) * nr * 8 + lane * 8);
+    const unsigned rl = ring_s + (unsigned)lane * 32u;
+    auto issue = [&](int i) {
+        if (i < nch && i * 32 + lane < nr) {
+            const unsigned d = rl + (unsigned)(i & (kBinRing - 1)) * 1024u;
+            const char *src = gsrc + (size_t)i * 1024;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 16u), "l"(src + 16) : "memory");
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < kBinRing - 2; ++i) issue(i);
+    int qn = 0;
+#ifndef FM_BIN_H
+#define FM_BIN_H 2
+#endif
+    constexpr int H = FM_BIN_H;   // chunks (of 32 realizations) per iteration
+    for (int i = 0; i < nch; i += H) {
+        issue(i + kBinRing - 2);
+        if (H == 2) issue(i + kBinRing - 1);
+        if (H == 2)
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(kBinRing - 2) : "memory");
+        else
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(kBinRing - 3) : "memory");
+        __syncwarp();
+        bool dq[H][NC];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const int r = (i + h) * 32 + lane;
+            const bool live = r < nr;
+            const unsigned ra = rl + (unsigned)((i + h) & (kBinRing - 1)) * 1024u;
+            float4 c0, c1;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(c0.x), "=f"(c0.y), "=f"(c0.z), "=f"(c0.w) : "r"(ra));
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(c1.x), "=f"(c1.y), "=f"(c1.z), "=f"(c1.w) : "r"(ra + 16u));
+            if (!live) {   // past N_rv: stale ring contents must not index the tables
+                c0 = make_float4(0.f, 0.f, 0.f, 0.f);
+                c1 = c0;
+            }
+            const float cf[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                float2 v = B[q].mu;
+#pragma unroll
+                for (int m = 0; m < 8; ++m) v = ffma2_bcast(cf[m], B[q].md[m], v);
+                const float2 z = K.bin_p1 ? v : f2_mul(v, ip2);
+                const float2 t1 = f2_add_rm(z, M2);             // M + floor(z)
+                const float2 f = f2_sub(z, f2_sub(t1, M2));     // frac(z) in [0, 1] (z finite: F_PROVEN)
+                const float2 tb = f2_fma_rm(f, NS2, M2);        // M + floor(frac * NS), <= M + NS
+                float2 ex, ey;   // (lo | kb + 1 in the low mantissa bits, hi)
+                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(ex.x), "=f"(ex.y) : "r"(tabx_s + 8u * (unsigned)__float_as_int(tb.x)));
+                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(ey.x), "=f"(ey.y) : "r"(taby_s + 8u * (unsigned)__float_as_int(tb.y)));
+                const int kbx = (__float_as_int(ex.x) & 63) - 1, kby = (__float_as_int(ey.x) & 63) - 1;
+                const int bx = (int)((unsigned)__float_as_int(t1.x) * (unsigned)k1x + cx[q] + (unsigned)kbx +
+                                     (f.x > ex.y ? 1u : 0u));
+                const int by = (int)((unsigned)__float_as_int(t1.y) * (unsigned)k1y + cy[q] + (unsigned)kby +
+                                     (f.y > ey.y ? 1u : 0u));
+                // safe: outside this bucket's zone on both axes and inside the box
+                const bool ok = live & ((f.x < ex.x) | (f.x > ex.y)) & ((f.y < ey.x) | (f.y > ey.y)) &
+                                ((unsigned)bx < (unsigned)bxn[q]) & ((unsigned)by < (unsigned)byn[q]);
+                if (ok) asm volatile("red.shared.add.u32 [%0], 1;\n" ::"r"(bb[q] + 4u * (unsigned)(by * bxn[q] + bx)) : "memory");
+                dq[h][q] = live & !ok;
+            }
+        }
+        bool any = false;
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+            for (int q = 0; q < NC; ++q) any |= dq[h][q];
+        if (__any_sync(kFull, any)) {
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    const unsigned bm = __ballot_sync(kFull, dq[h][q]);
+                    const int pos = qn + __popc(bm & ((1u << lane) - 1u));
+                    if (dq[h][q] && pos < kBinQ) bq[pos] = ((uint32_t)(p + q) << 16) | (uint32_t)((i + h) * 32 + lane);
+                    qn += __popc(bm);
+                }
+            if (qn > kBinQ) {   // too many doubtful realizations: per transition instead
+                cp_async_wait_all();
+                __syncwarp();
+                return -1;
+            }
+        }
+        __syncwarp();
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    return qn;
+}
+
+// A lean task by binning (see the comment at kBinNS).  Returns false when
+// some cell cannot be binned or too many realizations need the exact path;
+// the caller then runs the per-transition path (which clears its own
+// histogram).  On success the task's dense [slot][row] histogram -- at
+// wbase + off_bdense, over the coefficient ring -- holds exactly the counts
+// the per-transition path would produce.
+template <int FLAGS>
+__device__ __forceinline__ bool bin_task(const BuildK *__restrict__ Kg, unsigned char *wbase, const BinEnt *tab_s, int t,
+                                         int grp, int ag, const RowC &Rf, int outq, bool row_ok, int cs_row,
+                                         unsigned half_one)
+{
+    const BuildK &K = *Kg;
+    const int lane = threadIdx.x & 31;
+    const int CW = K.CW;
+    // every cell must fit before anything is written
+    for (int p = 0; p < CW; p += 2) {
+        int words = 0;
+        for (int q = 0; q < 2; ++q) {
+            const int cs = p + q, lc = grp * CW + cs;
+            if (cs < CW && lc < K.ncell) {
+                BinCell B;
+                int w;
+                if (!bin_setup(K, t, K.cell0 + lc, B, w)) return false;
+                words += w;
+            }
+        }
+        if (words > K.bin_words) return false;
+    }
+    uint32_t *bins = reinterpret_cast<uint32_t *>(wbase + K.off_bins);
+    uint32_t *bq = reinterpret_cast<uint32_t *>(wbase + K.off_bq);
+    const unsigned bins_s = (unsigned)__cvta_generic_to_shared(bins);
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(wbase + K.off_bdense);   // ring, then dense
+    uint16_t *h16 = reinterpret_cast<uint16_t *>(wbase + K.off_bdense) + lane;
+    uint16_t *h16q = h16 + Rf.soff * 32;
+    const unsigned hs_word = (unsigned)__cvta_generic_to_shared(h16q) & ~3u;
+    const int k1x = K.bin_k1x, k1y = K.bin_k1y;
+    const int a = ag * 32 + (lane - cs_row * K.AG);
+    for (int p = 0; p < CW; p += 2) {
+        BinCell B[2];
+        bool has[2];
+        int words = 0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int cs = p + q, lc = grp * CW + cs;
+            has[q] = cs < CW && lc < K.ncell;
+            int w = 0;
+            if (has[q]) bin_setup(K, t, K.cell0 + lc, B[q], w);
+            B[q].base = words;
+            words += w;
+            if (!has[q]) B[q].bx = B[q].by = B[q].offx = B[q].offy = 0;
+        }
+        for (int w = lane; w < words; w += 32) bins[w] = 0u;
+        __syncwarp();
+        const int qn = has[1] ? bin_loop<2>(K, B, p, t, tab_s, bins_s, ring_s, bq)
+                              : bin_loop<1>(K, B, p, t, tab_s, bins_s, ring_s, bq);
+        if (qn < 0) return false;
+        FM_STAT(5, lane == 0 ? 1 : 0);
+        // the ring is done: its space becomes the dense histogram (zeroed
+        // once, at the first pair), then the doubtful realizations go in
+        if (p == 0) {
+            for (int sl = 0; sl <= K.nslot; ++sl) h16[sl * 32] = 0;
+            __syncwarp();
+        }
+        for (int n = qn; n > 0;) n = bin_drain<FLAGS>(K, bq, n, t, grp, Rf, h16q, hs_word, outq, row_ok, cs_row, half_one);
+        asm volatile("" ::: "memory");
+        __syncwarp();
+        // 2-D inclusive prefix sums of each cell's bins (rows, then columns)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            uint32_t *b = bins + B[q].base;
+            for (int y = lane; y < B[q].by; y += 32) {
+                uint32_t acc = 0;
+                for (int x = 0; x < B[q].bx; ++x) {
+                    acc += b[y * B[q].bx + x];
+                    b[y * B[q].bx + x] = acc;
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            uint32_t *b = bins + B[q].base;
+            for (int x = lane; x < B[q].bx; x += 32) {
+                uint32_t acc = 0;
+                for (int y = 0; y < B[q].by; ++y) {
+                    acc += b[y * B[q].bx + x];
+                    b[y * B[q].bx + x] = acc;
+                }
+            }
+        }
+        __syncwarp();
+        // each row: its (di, dj) counts are rectangle sums over the bins
+        if (row_ok && (cs_row == p || cs_row == p + 1)) {
+            // the row's cell (selects keep B in registers: no dynamic index)
+            const bool q1 = cs_row == p + 1;
+            const int offx = q1 ? B[1].offx : B[0].offx, offy = q1 ? B[1].offy : B[0].offy;
+            const int cbx = q1 ? B[1].bx : B[0].bx, cby = q1 ? B[1].by : B[0].by;
+            const uint32_t *b = bins + (q1 ? B[1].base : B[0].base);
+            const BinAct ba = K.bact[a];
+            const int nxl = offx / k1x, nxh = nxl + cbx / k1x - 1;
+            const int nyl = offy / k1y, nyh = nyl + cby / k1y - 1;
+            const int dil = ba.gx + nxl + (ba.rx == 0 ? 1 : 0), dih = ba.gx + nxh + (ba.rx <= k1x - 1 ? 1 : 0);
+            const int djl = ba.gy + nyl + (ba.ry == 0 ? 1 : 0), djh = ba.gy + nyh + (ba.ry <= k1y - 1 ? 1 : 0);
+            for (int dj = djl; dj <= djh; ++dj) {
+                const int ey = dj - ba.gy;
+                const int y0 = max((ey - 1) * k1y + ba.ry - offy, 0);
+                const int y1 = min(ey * k1y + ba.ry - 1 - offy, cby - 1);
+                if (y0 > y1) continue;
+                for (int di = dil; di <= dih; ++di) {
+                    const int ex = di - ba.gx;
+                    const int x0 = max((ex - 1) * k1x + ba.rx - offx, 0);
+                    const int x1 = min(ex * k1x + ba.rx - 1 - offx, cbx - 1);
+                    if (x0 > x1) continue;
+                    uint32_t cnt = b[y1 * cbx + x1];
+                    if (x0 > 0) cnt -= b[y1 * cbx + x0 - 1];
+                    if (y0 > 0) cnt -= b[(y0 - 1) * cbx + x1];
+                    if (x0 > 0 && y0 > 0) cnt += b[(y0 - 1) * cbx + x0 - 1];
+                    if (cnt) {
+                        // inside the window by the F_PROVEN proof
+                        if ((unsigned)(di + K.hx) <= (unsigned)(2 * K.hx) && (unsigned)(dj + K.hy) <= (unsigned)(2 * K.hy))
+                            h16q[((Rf.cj + dj) * K.width + (Rf.ci + di)) * 32] += (uint16_t)cnt;
+                        else
+                            atomicOr(K.viol + (size_t)t * K.na + a, 2u);   // cannot happen: flags a bug loudly
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    return true;
+}
+
 // One warp = one task (t, group of CW source cells, group of <=32 actions).
 // Lane roles:
 //   row lane  (cs, a): owns the row (state t*N_c + c, action a); walks the
@@ -1356,17 +1890,31 @@ __device__ __forceinline__ void chunk_rows(const BuildK &K, const BuildK *__rest
 #define FM_BUILD_MINB 4
 #endif
 static_assert(FM_BUILD_RC <= 64, "chunk_rows_obst_cnt marks deferred realizations in a 64-bit mask");
+#ifndef FM_BUILD_MINB1
+#define FM_BUILD_MINB1 3
+#endif
 template <int FLAGS, int PART>
-__global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_constant__ BuildK K)
+__global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) ? FM_BUILD_MINB1
+                                                                                              : FM_BUILD_MINB)
+    k_build(const __grid_constant__ BuildK K)
 {
     const BuildK *__restrict__ Kg = &K;   // the parameter block, for the noinline rare paths
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char *wbase = smem + (size_t)warp * K.smem_warp;
+    unsigned char *wbase = smem + K.off_block + (size_t)warp * K.smem_warp;
+    // bin tables (lean tasks binned per realization): block-shared copy
+    const BinEnt *tab_s = reinterpret_cast<const BinEnt *>(smem);
+    if constexpr (PART == 1 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) {
+        if (K.bin_ok) {
+            BinEnt *t_s = reinterpret_cast<BinEnt *>(smem);
+            for (int i = threadIdx.x; i < 2 * (kBinNS + 1); i += blockDim.x) t_s[i] = K.tab[i];
+            __syncthreads();
+        }
+    }
     uint16_t *hist16 = (FLAGS & F_GHIST)                                     // [nslot+1][32]
                            ? K.ghist + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * (size_t)(K.nslot + 1) * 32
                            : reinterpret_cast<uint16_t *>(wbase);
-    uint16_t *h16 = hist16 + lane;
+    uint16_t *h16 = hist16 + lane;   // the task's dense histogram (a binned task moves it: bin_task)
     double2 *vbuf = reinterpret_cast<double2 *>(wbase + K.off_vbuf);       // [CW][RC+1]
     double *coefT = reinterpret_cast<double *>(wbase + K.off_coef);        // [nm][RC]
     double2 *modes_s = reinterpret_cast<double2 *>(wbase + K.off_modes);   // [CW][nm]
@@ -1396,6 +1944,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
         if (lane == 0) task = atomicAdd(K.task_counter, 1u);
         task = __shfl_sync(kFull, task, 0);
         if ((long long)task >= K.n_tasks) break;
+        h16 = hist16 + lane;
         const int per_t = K.groups * K.nag;
         const int t = K.t0 + (int)(task / per_t);
         const int rem = (int)(task % per_t);
@@ -1533,6 +2082,21 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
             Rf.tslot = R.tslot >= 0 ? R.tslot - R.soff : INT_MIN;
             const int outq = nslot - R.soff;
             uint16_t *h16q = h16 + R.soff * 32;
+            bool binned = false;
+            if constexpr (PART == 1 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) {
+                if (K.bin_ok) {
+                    binned = bin_task<FLAGS>(Kg, wbase, tab_s, t, grp, ag, Rf, outq, row_ok, cs_row, half_one);
+                    if (binned) {
+                        h16 = reinterpret_cast<uint16_t *>(wbase + K.off_bdense) + lane;
+                    } else {
+                        // the bin path's regions overlay this histogram: clear it
+                        if (lane == 0) FM_STAT(7, 1);
+                        for (int sl = 0; sl <= nslot; ++sl) h16[sl * 32] = 0;
+                        __syncwarp();
+                    }
+                }
+            }
+            if (!binned) {
             // stage the CW cells' modes
             for (int i = lane; i < CW * nm; i += 32) {
                 const int cs = i / nm, m = i - (i / nm) * nm;
@@ -1694,6 +2258,7 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
                 asm volatile("" ::: "memory");   // histogram reductions (no clobber) before any plain access
                 __syncwarp();
             }
+            }   // !binned
             const bool dead_row = row_ok && (R.rflags & RF_DEAD);
             if ((FLAGS & F_CNT) && dead_row) h16[nslot * 32] = (uint16_t)nr;   // every realization -> SINK
             if ((FLAGS & F_CNT) && row_ok && edge_row && !dead_row) {
@@ -1758,6 +2323,13 @@ __global__ void __launch_bounds__(128, FM_BUILD_MINB) k_build(const __grid_const
             }
         }
         __syncwarp();
+        if (PART == 1 && h16 != hist16 + lane) {
+            // a binned task: its counters overlaid the per-transition
+            // histogram, which every task expects zeroed
+            uint4 *z = reinterpret_cast<uint4 *>(hist16);
+            for (int i = lane; i < (nslot + 1) * 4; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();
+        }
     }
 }
 
@@ -1862,6 +2434,27 @@ static void smem_layout_fit(BuildK &K, int queue, bool hg)
     smem_layout(K, cands[best], queue, hg);
 }
 
+// Per-warp regions of the bin path, overlaid on the legacy layout after the
+// dense histogram: bin counters | coefficient ring | deferred queue.  The
+// counters take whatever the legacy layout leaves (at least 512 words), so
+// the bin path costs no occupancy when it fits.
+static void bin_layout(BuildK &K)
+{
+    const int ring = kBinRing * 32 * 32, dense = (K.nslot + 1) * 64, q = kBinQ * 4;
+    const int uni = align16(ring > dense ? ring : dense);
+    K.off_bins = 0;
+    int words = ((K.smem_warp - uni - q) / 4) & ~31;
+    const char *ev = getenv("FM_BIN_WORDS");   // dev override (A/B of the occupancy trade-off)
+    const int floor_words = ev ? atoi(ev) : (K.CW >= 2 ? 1024 : 2048);
+    if (words < floor_words) words = floor_words;
+    K.bin_words = words;
+    K.off_bdense = align16(words * 4);
+    K.off_bq = K.off_bdense + uni;
+    const int end = align16(K.off_bq + q);
+    if (end > K.smem_warp) K.smem_warp = end;
+    K.off_block = align16(2 * (kBinNS + 1) * (int)sizeof(BinEnt));
+}
+
 template <int FL, int PART>
 static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
 {
@@ -1876,14 +2469,14 @@ static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
             max_block = 232448;
         cudaGetLastError();
     }
-    int wpb = max_block / K.smem_warp;
+    int wpb = (max_block - K.off_block) / K.smem_warp;
     if (wpb > 4) wpb = 4;
     if (wpb < 1)
         return fm_fail(FM_BAD_ARG,
                        "sub-grid of %d slots needs %d B of shared memory per warp (at most %d per block on this "
                        "device)",
                        K.nslot + 1, K.smem_warp, max_block);
-    const size_t bytes = (size_t)wpb * K.smem_warp;
+    const size_t bytes = (size_t)K.off_block + (size_t)wpb * K.smem_warp;
     FM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     int occ = 0;
     FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * wpb, bytes));
@@ -1905,6 +2498,7 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
             // lean net-energy rows read h_cr * g[t+1] from a per-warp slot
             // table (half-size chunks keep 4 blocks per SM)
             BuildK K1 = K;
+            K1.off_block = 0;
             smem_layout_fit(K1, 0, true);
             st = launch_build_p<FL, 1>(K1, (size_t)4 * K1.smem_warp, s);
         } else {
@@ -1915,10 +2509,13 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
             // obstacle part: per-warp queue of deferred exact segment tests
             // (half-size reconstruction chunks keep it at 4 blocks per SM)
             BuildK K2 = K;
+            K2.off_block = 0;
             smem_layout_fit(K2, kQueue, false);
             return launch_build_p<FL, 2>(K2, (size_t)4 * K2.smem_warp, s);
         } else {
-            return launch_build_p<FL, 2>(K, smem, s);
+            BuildK K2 = K;
+            K2.off_block = 0;
+            return launch_build_p<FL, 2>(K2, smem, s);
         }
     }
 }
@@ -2096,6 +2693,134 @@ static bool rewards_sum_exactly(const fm_build_args *h)
     return ldexp(mx, K) * (double)h->env.n_real <= 0x1p52;
 }
 
+// Bin structure of one axis (see kBinNS): per action gamma / cluster index,
+// clusters of step positions theta_a in (0, 1) and the bucket table.  Steps
+// closer than 2 dzone + a bucket (plus margin) apart share one cluster, whose
+// zone [min - dzone, max + dzone] routes realizations to the exact path, so
+// every realization outside all zones lies on one side of every step of the
+// cluster; steps near 0 or 1 join the unit boundary (always / never).
+static bool bin_axis(const std::vector<double> &comp, double p, double dz, int &k1, BinEnt *tab, int *g, int *r)
+{
+    const double eta = 1.0 / (8.0 * kBinNS), gap = 1.0 / kBinNS + 2.0 * eta;
+    double hi0 = dz, lotop = 1.0 - dz;
+    std::vector<int> bottom, top;
+    std::vector<std::pair<double, int>> th;
+    for (size_t a = 0; a < comp.size(); ++a) {
+        const double c = 0.5 + comp[a] / p;
+        if (!std::isfinite(c) || fabs(c) > 0x1p20) return false;
+        const double gam = floor(c), beta = c - gam;
+        g[a] = (int)gam;
+        const double theta = beta > 0.0 ? 1.0 - beta : 1.0;
+        if (theta <= 2.0 * dz + gap) {
+            bottom.push_back((int)a);
+            hi0 = fmax(hi0, theta + dz);
+        } else if (theta >= 1.0 - 2.0 * dz - gap) {
+            top.push_back((int)a);
+            lotop = fmin(lotop, theta - dz);
+        } else {
+            th.push_back({theta, (int)a});
+        }
+    }
+    std::sort(th.begin(), th.end());
+    std::vector<double> clo, chi;
+    std::vector<std::vector<int>> mem;
+    for (auto &e : th) {
+        if (!clo.empty() && e.first - dz - chi.back() <= gap) {
+            chi.back() = e.first + dz;
+            mem.back().push_back(e.second);
+        } else {
+            clo.push_back(e.first - dz);
+            chi.push_back(e.first + dz);
+            mem.push_back({e.second});
+        }
+    }
+    while (!clo.empty() && clo.front() - hi0 <= gap) {
+        hi0 = fmax(hi0, chi.front());
+        bottom.insert(bottom.end(), mem.front().begin(), mem.front().end());
+        clo.erase(clo.begin()); chi.erase(chi.begin()); mem.erase(mem.begin());
+    }
+    while (!clo.empty() && lotop - chi.back() <= gap) {
+        lotop = fmin(lotop, clo.back());
+        top.insert(top.end(), mem.back().begin(), mem.back().end());
+        clo.pop_back(); chi.pop_back(); mem.pop_back();
+    }
+    if (!(hi0 + gap < lotop)) return false;
+    const int K = (int)clo.size();
+    k1 = K + 1;
+    for (int a : bottom) r[a] = 0;
+    for (int a : top) r[a] = K + 1;
+    for (int k = 0; k < K; ++k)
+        for (int a : mem[k]) r[a] = k + 1;
+    if (K + 2 > 63) return false;   // kb + 1 must fit the 6 packed bits
+    auto rd = [](double x) { return std::nextafter((float)x, -INFINITY); };
+    auto ru = [](double x) { return std::nextafter((float)x, INFINITY); };
+    // lo rounded down past its low 6 mantissa bits, which then carry kb + 1
+    auto pack = [](float lo, int kb) {
+        int b;
+        memcpy(&b, &lo, 4);
+        b = lo >= 0.0f ? ((b - 64) & ~63) : ((b + 64) & ~63);   // smaller value either way
+        b |= kb + 1;
+        float r;
+        memcpy(&r, &b, 4);
+        return r;
+    };
+    for (int b = 0; b <= kBinNS; ++b) {   // entry NS: frac == 1
+        const double elo = (double)b / kBinNS - eta, ehi = (double)(b + 1) / kBinNS + eta;
+        int kb = 0;
+        for (int k = 0; k < K; ++k) kb += chi[k] < elo ? 1 : 0;
+        float lo = 3.0f, hi = 3.0f;
+        int hits = 0;
+        if (hi0 >= elo) { kb = -1; lo = -1.0f; hi = ru(hi0); ++hits; }
+        for (int k = 0; k < K; ++k)
+            if (clo[k] <= ehi && chi[k] >= elo) { kb = k; lo = rd(clo[k]); hi = ru(chi[k]); ++hits; }
+        if (lotop <= ehi) { kb = K; lo = rd(lotop); hi = 2.0f; ++hits; }
+        if (hits > 1) return false;
+        tab[b] = BinEnt{pack(lo, kb), hi};
+    }
+    return true;
+}
+
+// Enables the bin path for a proven, count-formed build: tables, error
+// allowances, per-action parameters.  dzone is sized for a reconstruction
+// magnitude T of 3 vmax + 1; cells with a larger bound take the
+// per-transition path (bin_setup).
+static void bin_params(const fm_build_args *h, BuildK &K)
+{
+    K.bin_ok = 0;
+    const fm_grid &G = h->grid;
+    // at most two cells per task: the dense histogram overlays the
+    // coefficient ring, so a task's cells are binned in one pass
+    if (K.nm > 8 || K.na > kBinMaxA || K.CW > 2 || !h->h_actions) return;
+    const double p = G.dx / G.dt;
+    if (!(p > 0.0) || !std::isfinite(p)) return;
+    const double vmax = fmax(h->vmax_x, h->vmax_y);
+    double amax = 0.0;
+    std::vector<double> ax(K.na), ay(K.na);
+    for (int a = 0; a < K.na; ++a) {
+        ax[a] = h->h_actions[a].ax;
+        ay[a] = h->h_actions[a].ay;
+        amax = fmax(amax, fmax(fabs(ax[a]), fabs(ay[a])));
+    }
+    // the reference's own roundings in the landing index (cell units): a
+    // handful of roundings of magnitudes below M / dx
+    const double M = fmax(fmax(fabs(G.ox), fabs(G.ox + G.nx * G.dx)), fmax(fabs(G.oy), fabs(G.oy + G.ny * G.dx))) +
+                     (vmax + amax) * G.dt + G.dx;
+    K.bin_eps = 0x1p-48 * (M / G.dx + 2.0);
+    const double T = 3.0 * vmax + 1.0, ip = 1.0 / p;
+    const double kRel = (2.0 * K.nm + 8.0) * 0x1p-24 * 1.001;
+    K.bin_dzone = fmax(0x1p-17, 2.0 * (T * kRel * ip + 0x1p-21 * (T * ip + 1.0) + K.bin_eps));
+    std::vector<int> gx(K.na), rx(K.na), gy(K.na), ry(K.na);
+    if (!bin_axis(ax, p, K.bin_dzone, K.bin_k1x, K.tab, gx.data(), rx.data())) return;
+    if (!bin_axis(ay, p, K.bin_dzone, K.bin_k1y, K.tab + kBinNS + 1, gy.data(), ry.data())) return;
+    for (int a = 0; a < K.na; ++a) K.bact[a] = BinAct{gx[a], rx[a], gy[a], ry[a]};
+    K.bin_p = p;
+    K.bin_p1 = p == 1.0 ? 1 : 0;
+    K.bin_ip = (float)ip;
+    K.envelope = reinterpret_cast<const int4 *>(h->envelope);
+    K.bin_ok = 1;
+    bin_layout(K);
+}
+
 // validates the arguments and fills the kernel parameter block + flags
 static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K, int &flags)
 {
@@ -2115,6 +2840,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     if (h->reward.target_i < 0 || h->reward.target_i >= G.nx || h->reward.target_j < 0 || h->reward.target_j >= G.ny)
         return fm_fail(FM_BAD_ARG, "target cell (%d, %d) outside grid", h->reward.target_i, h->reward.target_j);
 
+    K = BuildK{};
     K.nx = G.nx; K.ny = G.ny; K.nt = G.nt; K.nc = G.nx * G.ny;
     K.dx = G.dx; K.dt = G.dt; K.ox = G.ox; K.oy = G.oy;
     K.inv_dx = 1.0 / G.dx;
@@ -2179,7 +2905,37 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
         smem_layout(K, K.RW >= 32 ? K.RW : 32, 0, false, true);
         flags = (flags & F_NET) | F_GHIST;
     }
+    if ((flags & F_PROVEN) && (flags & F_CNT) && !(flags & F_GHIST) && !getenv("FM_NO_BINS")) {
+        bin_params(h, K);
+        if (K.bin_ok && K.off_block + K.smem_warp > smem_block_optin()) {   // no room: per transition
+            K.bin_ok = 0;
+            K.off_block = 0;
+            smem_layout_fit(K, 0, false);
+        }
+    }
     return FM_OK;
+}
+
+// Bin path inputs for slabs [t0, t1): f32 coefficients padded to 8 modes
+// ([t - t0][r][8]) and max_r |coeff| per (t, m) (the error bound's T).
+__global__ void k_bin_prep(const double *coeffs, int t0, int nts, int nr, int nm, float *c32, double *cmax)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)nts * nr) return;
+    const int tl = (int)(i / nr);
+    const double *src = coeffs + ((size_t)(t0 + tl) * nr + (i % nr)) * nm;
+    float out[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const double c = m < nm ? src[m] : 0.0;
+        out[m] = (float)c;
+        if (m < nm)
+            atomicMax(reinterpret_cast<unsigned long long *>(cmax + (size_t)tl * nm + m),
+                      (unsigned long long)__double_as_longlong(fabs(c)));   // non-negative: bits order
+    }
+    float4 *dst = reinterpret_cast<float4 *>(c32 + (size_t)i * 8);
+    dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+    dst[1] = make_float4(out[4], out[5], out[6], out[7]);
 }
 
 extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *stream)
@@ -2192,7 +2948,23 @@ extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *st
     st = frac_table_init();
     if (st != FM_OK) return st;
     FM_CK(cudaMemsetAsync(h->task_counter, 0, sizeof(unsigned int), s));
-    return launch_build(K, flags, (size_t)4 * K.smem_warp, s);
+    float *c32 = nullptr;
+    double *cmax = nullptr;
+    if (K.bin_ok) {
+        const int nts = K.t1 - K.t0;
+        FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&c32), sizeof(float) * 8 * (size_t)nts * K.nr, s));
+        FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&cmax), sizeof(double) * (size_t)nts * (K.nm ? K.nm : 1), s));
+        FM_CK(cudaMemsetAsync(cmax, 0, sizeof(double) * (size_t)nts * (K.nm ? K.nm : 1), s));
+        const long long n = (long long)nts * K.nr;
+        k_bin_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(K.coeffs, K.t0, nts, K.nr, K.nm, c32, cmax);
+        FM_CK_LAUNCH("k_bin_prep");
+        K.coef32 = c32;
+        K.cmax = cmax;
+    }
+    st = launch_build(K, flags, (size_t)4 * K.smem_warp, s);
+    if (c32) FM_CK(cudaFreeAsync(c32, s));
+    if (cmax) FM_CK(cudaFreeAsync(cmax, s));
+    return st;
 }
 
 extern "C" int32_t fm_build_check(const fm_build_args *h, fm_model *M, uint64_t *h_needed, fm_violation *h_viol,
@@ -2985,6 +3757,7 @@ extern "C" int32_t fm_rollout(const fm_rollout_args *h, void *stream)
     if (h->n_traj == 0) return FM_OK;
     RollK R{};
     BuildK &K = R.B;
+    K = BuildK{};
     K.nx = G.nx; K.ny = G.ny; K.nt = G.nt; K.nc = G.nx * G.ny;
     K.dx = G.dx; K.dt = G.dt; K.ox = G.ox; K.oy = G.oy;
     K.inv_dx = 1.0 / G.dx;

@@ -420,3 +420,38 @@ def test_scanned_upload_matches_full_scan(slabs):
         pinned.obstacles = type("O", (), {"mask": torch.from_numpy(env.obstacles.mask.view(np.uint8)).pin_memory()})()
         dp = DeviceEnv.from_host_scanned(pinned, slabs=slabs)
         assert torch.equal(dp.modes, ref.modes) and dp.velocity_max() == full
+
+
+@pytest.mark.parametrize("case", ["desk", "paper_1k", "zero_flow", "random"])
+def test_binned_build_equals_per_transition_build(case, monkeypatch):
+    """Lean cells binned per (cell, realization) (k_build's bin path, with
+    the scan's per-cell envelope or the in-kernel triangle bound) give the
+    same model as the per-transition path (FM_NO_BINS), entry for entry."""
+    import torch
+    if case == "desk":
+        env, acts, rcfg, target, _ = make_named_env("desk")
+    elif case == "paper_1k":
+        from paper_2109_00857_b200 import workloads
+        w = workloads.get("paper").with_(n_realizations=1000)
+        env, acts, rcfg, target = w.environment(), w.actions(), w.reward_config(), w.target
+    elif case == "zero_flow":   # every realization sits exactly on a step: all take the exact path
+        env = make_zero_flow_env(nx=12, ny=12, nt=5, n_realizations=64)
+        acts, rcfg, target = ActionSpace(8, 2, 1.0), RewardConfig("time", r_term=10.0, r_outbound=-50.0), (9, 9)
+    else:
+        env, acts, rcfg, target = make_random_env(7005)
+    denv = DeviceEnv.from_host(env)
+    sub = fm.compute_subgrid(env.field, acts, env.grid, device_env=denv)
+
+    def flat(dm):
+        sm = dm.to_sparse_model()
+        return model_digest(sm), sm.rewards.tobytes()
+
+    binned = flat(build_device_model(denv, acts, rcfg, target, sub))
+    saved = denv._env_rows
+    denv._env_rows = None                     # no envelope: triangle bound around the mean
+    tri = flat(build_device_model(denv, acts, rcfg, target, sub))
+    denv._env_rows = saved
+    monkeypatch.setenv("FM_NO_BINS", "1")
+    ref = flat(build_device_model(denv, acts, rcfg, target, sub))
+    assert binned == ref and tri == ref
+    torch.cuda.synchronize()

@@ -15,5 +15,5 @@ L.fm_dev_stats(out)
 dm = build_device_model(de, w.actions(), w.reward_config(), w.target, sub)
 torch.cuda.synchronize()
 L.fm_dev_stats(out)
-names = ["rare", "seg_exact", "seg_samples", "obst_trans", "lean_trans"]
+names = ["rare", "seg_exact", "seg_samples", "obst_trans", "lean_trans", "bin_tasks", "bin_exact", "bin_misfit"]
 print(name, {n: int(out[i]) for i, n in enumerate(names)}, "U", w.transitions)
