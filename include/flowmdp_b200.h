@@ -78,7 +78,10 @@ typedef struct {
 } fm_reward;
 
 /* Device-resident compact model produced by fm_build.
- * Rows are (t, c, a) with row id = (t*N_c + c)*n_actions + a.
+ * Rows are (t, c, a) for the cells c of [cell0, cell0 + ncell) -- the
+ * whole layer (cell0 = 0, ncell = N_c) or one GPU's row strip (rows j0..j1:
+ * cell0 = j0*nx, ncell = (j1-j0)*nx) -- with
+ * row id = (t*ncell + c - cell0)*n_actions + a.
  * Entry word = (slot << 16) | count; slot indexes the (2hx+1)(2hy+1)
  * displacement window row-major in (dj, di), slot == n_slots is the OUT
  * slot (successor SINK).  probability = count / n_real.
@@ -87,7 +90,8 @@ typedef struct {
 typedef struct {
     int32_t nx, ny, nt, n_actions, n_real;
     int32_t hx, hy;            /* sub-grid half widths used for slots        */
-    int64_t n_rows;            /* nt*N_c*n_actions                           */
+    int32_t cell0, ncell;      /* cells whose rows the model holds           */
+    int64_t n_rows;            /* nt*ncell*n_actions                         */
     uint64_t *row_ptr;         /* [n_rows] first entry of each row           */
     uint16_t *row_nnz;         /* [n_rows]                                   */
     double *reward;            /* [n_rows] R_{a,t}[s] = sum_r / n_real       */
@@ -132,6 +136,11 @@ typedef struct {
      * (cell, action, realization): each realization is binned once against
      * the action set's landing thresholds; the counts are unchanged. */
     const int32_t *envelope;
+    /* SMs' worth of thread blocks the persistent build grid leaves free, so
+     * kernels on other streams (a pipelined backward solve, the halo
+     * exchange's communication kernels) run while the build proceeds.  0 =
+     * the whole GPU. */
+    int32_t reserve_sms;
 } fm_build_args;
 
 /* Sub-grid overflow report (message of model_builder.py:433-438). */

@@ -79,6 +79,7 @@ class FmReward(C.Structure):
 class FmModel(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nt", C.c_int32), ("n_actions", C.c_int32),
                 ("n_real", C.c_int32), ("hx", C.c_int32), ("hy", C.c_int32),
+                ("cell0", C.c_int32), ("ncell", C.c_int32),
                 ("n_rows", C.c_int64),
                 ("row_ptr", C.c_void_p), ("row_nnz", C.c_void_p), ("reward", C.c_void_p),
                 ("entries", C.c_void_p), ("capacity", C.c_uint64), ("d_nnz", C.c_void_p)]
@@ -92,7 +93,7 @@ class FmBuildArgs(C.Structure):
                 ("t0", C.c_int32), ("t1", C.c_int32), ("j0", C.c_int32), ("j1", C.c_int32),
                 ("viol_flags", C.c_void_p), ("task_counter", C.c_void_p), ("d_gate_r", C.c_void_p),
                 ("h_actions", C.c_void_p), ("vmax_x", C.c_double), ("vmax_y", C.c_double),
-                ("envelope", C.c_void_p)]
+                ("envelope", C.c_void_p), ("reserve_sms", C.c_int32)]
 
 
 class FmViolation(C.Structure):

@@ -373,8 +373,28 @@ class DeviceModel:
     j_range: tuple
 
     @property
+    def cell0(self) -> int:
+        """First cell whose rows the model holds (row strip j_range)."""
+        return self.j_range[0] * self.grid.nx
+
+    @property
+    def ncell(self) -> int:
+        return (self.j_range[1] - self.j_range[0]) * self.grid.nx
+
+    @property
     def n_rows(self) -> int:
-        return self.grid.nt * self.grid.nx * self.grid.ny * self.n_actions
+        """Rows (t, c, a) of every layer for the strip's cells only:
+        row id = (t * ncell + c - cell0) * n_actions + a."""
+        return self.grid.nt * self.ncell * self.n_actions
+
+    def row_ids(self, t: int, a: int, j0: int, j1: int):
+        """Device row ids of action a, layer t, source rows j in [j0, j1)."""
+        torch = _torch()
+        g = self.grid
+        if not (self.j_range[0] <= j0 and j1 <= self.j_range[1]):
+            raise ContractViolation(f"rows [{j0}, {j1}) are not in this model (rows {self.j_range})")
+        cells = torch.arange(j0 * g.nx, j1 * g.nx, device=self.row_ptr.device, dtype=torch.int64)
+        return cells, (t * self.ncell + cells - self.cell0) * self.n_actions + a
 
     @property
     def nt(self) -> int:
@@ -386,6 +406,7 @@ class DeviceModel:
 
     _pending: tuple | None = None
     _scratch: tuple | None = None
+    group_events: list = field(default_factory=list)   # ((t0, t1), cuda event) per launch group
 
     def check(self) -> bool:
         """Finish a (deferred) build: census, sub-grid overflow (raises the
@@ -421,7 +442,7 @@ class DeviceModel:
         g = self.grid
         return _lib.FmModel(g.nx, g.ny, g.nt, self.n_actions, self.n_real,
                             self.subgrid.half_width_x, self.subgrid.half_width_y,
-                            self.n_rows, self.row_ptr.data_ptr(), self.row_nnz.data_ptr(),
+                            self.cell0, self.ncell, self.n_rows, self.row_ptr.data_ptr(), self.row_nnz.data_ptr(),
                             self.reward.data_ptr(), self.entries.data_ptr(),
                             int(self.entries.numel()), self.d_nnz.data_ptr())
 
@@ -434,8 +455,7 @@ class DeviceModel:
         self.check()
         g, na = self.grid, self.n_actions
         nc = g.nx * g.ny
-        cells = torch.arange(j0 * g.nx, j1 * g.nx, device=self.row_ptr.device, dtype=torch.int64)
-        rid = (t * nc + cells) * na + a
+        cells, rid = self.row_ids(t, a, j0, j1)
         ptr = self.row_ptr[rid]
         cnt = self.row_nnz[rid].to(torch.int64) & 0xFFFF
         idx = torch.repeat_interleave(ptr, cnt) + (torch.arange(int(cnt.sum()), device=ptr.device)
@@ -496,7 +516,8 @@ class DeviceModel:
 def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridSpec,
                        t_range: tuple | None = None, j_range: tuple | None = None,
                        capacity_hint: int | None = None, defer_check: bool = False,
-                       lean: bool = True, reuse: DeviceModel | None = None) -> DeviceModel:
+                       lean: bool = True, reuse: DeviceModel | None = None,
+                       t_groups: list | None = None, reserve_sms: int = 0) -> DeviceModel:
     """Run K_build over slabs t_range x row strip j_range; the model stays in HBM.
 
     With defer_check the kernel is only enqueued: consumers (the backward
@@ -510,7 +531,13 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
 
     ``reuse`` hands over the buffers of a previous model of the same problem
     shape (that model must not be used afterwards): repeated planner steps
-    then allocate nothing."""
+    then allocate nothing.
+
+    ``t_groups`` (slab ranges covering t_range, in launch order -- for the
+    pipelined solve, descending): one launch per group on the current
+    stream, an event recorded after each (``DeviceModel.group_events``), so
+    a solve stream can start on a group's layers while later groups build;
+    ``reserve_sms`` leaves that many SMs' worth of blocks free for it."""
     torch = _torch()
     L = _lib.load()
     grid = denv.grid
@@ -519,7 +546,7 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
         raise ContractViolation(f"target cell {tuple(target)} outside grid")
     t0, t1 = t_range if t_range is not None else (0, grid.nt)
     j0, j1 = j_range if j_range is not None else (0, grid.ny)
-    full = (t0, t1) == (0, grid.nt) and (j0, j1) == (0, grid.ny)
+    full = (t0, t1) == (0, grid.nt)   # every row of the strip is written
     dev = denv.mean.device
     recs = action_records(actions, rcfg, grid)
     na = recs.shape[0]
@@ -527,11 +554,12 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     d_gate = denv.gate_radius_device(float(actions.f_max))
     hx, hy = subgrid.half_width_x, subgrid.half_width_y
     nc = grid.nx * grid.ny
-    n_rows = grid.nt * nc * na
+    n_rows = grid.nt * (j1 - j0) * grid.nx * na   # the strip's rows only (all layers)
     active_rows = (t1 - t0) * (j1 - j0) * grid.nx * na
     n_slot1 = (2 * hx + 1) * (2 * hy + 1) + 1
     cap = capacity_hint if capacity_hint else active_rows * min(n_slot1, denv.n_real, 6) + 1024
-    if reuse is not None and reuse.row_ptr.numel() == n_rows and reuse.row_ptr.device == dev:
+    if reuse is not None and reuse.row_ptr.numel() == n_rows and reuse.row_ptr.device == dev and \
+            reuse.j_range == (j0, j1):
         row_ptr, row_nnz, reward, d_nnz = reuse.row_ptr, reuse.row_nnz, reuse.reward, reuse.d_nnz
         d_nnz.zero_()
         if not full:
@@ -559,7 +587,7 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     args = _lib.FmBuildArgs(denv.fm_grid(), denv.fm_env(), rw, d_act.data_ptr(), na, hx, hy, 0, 0,
                             denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr(),
                             d_gate.data_ptr(), recs.ctypes.data if lean else None, vmx, vmy,
-                            denv.envelope_for(j0, j1) if lean else None)
+                            denv.envelope_for(j0, j1) if lean else None, int(reserve_sms))
     if entries is None:
         entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
     dm = DeviceModel(grid=grid, n_actions=na, n_real=denv.n_real, subgrid=subgrid,
@@ -568,7 +596,19 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     dm._pending = (args, (d_act, d_gate, viol, counter, denv, recs))
     dm._scratch = (viol, counter)
     m = dm.fm_model()
-    _lib.check(L.fm_build_launch(C.byref(args), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
+    dm.group_events = []
+    if t_groups:
+        if sorted(t for g in t_groups for t in range(*g)) != list(range(t0, t1)):
+            raise ContractViolation("t_groups must partition the slab range")
+        for g0, g1 in t_groups:
+            ga = _lib.FmBuildArgs.from_buffer_copy(args)
+            ga.t0, ga.t1 = int(g0), int(g1)
+            _lib.check(L.fm_build_launch(C.byref(ga), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
+            ev = torch.cuda.Event()
+            ev.record()
+            dm.group_events.append(((int(g0), int(g1)), ev))
+    else:
+        _lib.check(L.fm_build_launch(C.byref(args), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
     if not defer_check:
         dm.check()
     return dm

@@ -688,7 +688,9 @@ struct BuildK {
     int smem_warp, off_vbuf, off_coef, off_modes, off_danger;
     int off_queue;   // PART 2 (F_PROVEN | F_CNT): deferred exact-test queue [kQueue]
     int off_hg;      // PART 1 (F_PROVEN | F_NET): h_cr * g[t+1] per (cell, window slot)
-    // outputs
+    // outputs: rows of the model's cells [mcell0, mcell0 + mncell)
+    int mcell0, mncell;
+    int reserve_sms;    // SMs' worth of blocks left free for other streams
     uint64_t *row_ptr;
     uint16_t *row_nnz;
     double *reward;
@@ -2310,7 +2312,7 @@ __global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAG
         base_pos = __shfl_sync(kFull, base_pos, 0);
         if (row_ok) {
             unsigned long long pos = base_pos + (unsigned long long)(incl - nnz);
-            const size_t row = ((size_t)t * K.nc + c) * K.na + a;
+            const size_t row = ((size_t)t * K.mncell + (c - K.mcell0)) * K.na + a;
             K.row_ptr[row] = pos;
             K.row_nnz[row] = (uint16_t)nnz;
             K.reward[row] = DDIV(S, (double)nr);   // finalize_rewards (model_builder.py:462-464)
@@ -2482,7 +2484,9 @@ static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
     FM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * wpb, bytes));
     if (occ < 1) return fm_fail(FM_BAD_ARG, "k_build: %zu B smem per block does not fit", bytes);
     FM_CK(cudaMemsetAsync(K.task_counter, 0, sizeof(unsigned int), s));
-    kern<<<occ * sm_count(), 32 * wpb, bytes, s>>>(K);
+    int sms = sm_count() - K.reserve_sms;
+    if (sms < 1) sms = 1;
+    kern<<<occ * sms, 32 * wpb, bytes, s>>>(K);
     FM_CK_LAUNCH("k_build");
     return FM_OK;
 }
@@ -2837,6 +2841,11 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
         return fm_fail(FM_BAD_ARG, "fm_build: bad slab/strip range");
     if (M->n_actions != h->n_actions || M->nt != G.nt || M->nx != G.nx || M->ny != G.ny)
         return fm_fail(FM_BAD_ARG, "fm_build: model header does not match the problem");
+    if (M->cell0 < 0 || M->ncell < 1 || M->cell0 + M->ncell > G.nx * G.ny ||
+        M->n_rows != (int64_t)G.nt * M->ncell * h->n_actions)
+        return fm_fail(FM_BAD_ARG, "fm_build: model rows do not match its cell range");
+    if (h->j0 * G.nx < M->cell0 || h->j1 * G.nx > M->cell0 + M->ncell)
+        return fm_fail(FM_BAD_ARG, "fm_build: rows [%d, %d) are outside the model's cells", h->j0, h->j1);
     if (h->reward.target_i < 0 || h->reward.target_i >= G.nx || h->reward.target_j < 0 || h->reward.target_j >= G.ny)
         return fm_fail(FM_BAD_ARG, "target cell (%d, %d) outside grid", h->reward.target_i, h->reward.target_j);
 
@@ -2871,6 +2880,9 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.sx_hi = -1;
     K.sy_lo = G.ny;
     K.sy_hi = -1;
+    K.mcell0 = M->cell0; K.mncell = M->ncell;
+    K.mcell0 = M->cell0; K.mncell = M->ncell;
+    K.reserve_sms = h->reserve_sms > 0 ? h->reserve_sms : 0;
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward;
     K.entries = M->entries; K.capacity = M->capacity;
     K.nnz_counter = reinterpret_cast<unsigned long long *>(M->d_nnz);
@@ -3118,6 +3130,7 @@ static int32_t scan_u64(uint64_t *data, int64_t n, cudaStream_t s)
 // ---------------------------------------------------------------------------
 struct ModelK {
     int nx, ny, nt, nc, na, nr, hx, hy, width, nslot;
+    int cell0, ncell;   // cells whose rows the model holds (row = (t*ncell + c - cell0)*na + a)
     long long n_rows, n_g;
     unsigned long long capacity;
     const uint64_t *row_ptr;
@@ -3132,6 +3145,7 @@ static ModelK model_k(const fm_model *M)
     K.nx = M->nx; K.ny = M->ny; K.nt = M->nt; K.nc = M->nx * M->ny; K.na = M->n_actions;
     K.nr = M->n_real; K.hx = M->hx; K.hy = M->hy; K.width = 2 * M->hx + 1;
     K.nslot = (2 * M->hx + 1) * (2 * M->hy + 1);
+    K.cell0 = M->cell0; K.ncell = M->ncell;
     K.n_rows = M->n_rows; K.n_g = (long long)M->nt * K.nc;
     K.row_ptr = M->row_ptr; K.row_nnz = M->row_nnz; K.reward = M->reward; K.entries = M->entries;
     K.capacity = M->capacity;
@@ -3190,6 +3204,8 @@ extern "C" int32_t fm_export_coo(const fm_model *M, uint64_t *d_scratch, uint64_
     cudaStream_t s = (cudaStream_t)stream;
     const ModelK K = model_k(M);
     if (K.n_rows <= 0) return fm_fail(FM_BAD_ARG, "fm_export_coo: empty model");
+    if (K.cell0 != 0 || K.ncell != K.nc)
+        return fm_fail(FM_BAD_ARG, "fm_export_coo: needs a model of whole layers (this one holds a row strip)");
     const unsigned nb = (unsigned)((K.n_rows + 255) / 256);
     k_export_count<<<nb, 256, 0, s>>>(K, d_scratch);
     FM_CK_LAUNCH("k_export_count");
@@ -3253,7 +3269,7 @@ __global__ void __launch_bounds__(256) k_solve_layer(const SolveK S)
     for (int ag = 0; ag < S.nag; ++ag) {
         const int a = ag * 32 + a_loc;
         if (cell_ok && a < K.na) {
-            const size_t row = ((size_t)t * K.nc + c) * K.na + a;
+            const size_t row = ((size_t)t * K.ncell + (c - K.cell0)) * K.na + a;
             const uint64_t p = K.row_ptr[row];
             // an over-capacity build (deferred check) is discarded; never read past the buffer
             const int n = p + K.row_nnz[row] <= K.capacity ? K.row_nnz[row] : 0;
@@ -3296,6 +3312,8 @@ static int32_t solve_layer(const fm_model *M, const double *ptab, int t, int j0,
     S.t = t;
     S.cell0 = j0 * M->nx;
     S.ncell = (j1 - j0) * M->nx;
+    if (S.cell0 < M->cell0 || S.cell0 + S.ncell > M->cell0 + M->ncell)
+        return fm_fail(FM_BAD_ARG, "solve: rows [%d, %d) are not in the model", j0, j1);
     S.AG = M->n_actions < 32 ? M->n_actions : 32;
     S.nag = (M->n_actions + 31) / 32;
     S.CW = 32 / S.AG;
@@ -3350,8 +3368,9 @@ extern "C" int32_t fm_solve_backward(const fm_model *M, int32_t t_lo, int32_t t_
     int32_t st;
     double *ptab = prob_table(M, s, &st);
     if (st != FM_OK) return st;
+    if (M->ncell % M->nx || M->cell0 % M->nx) return fm_fail(FM_BAD_ARG, "fm_solve_backward: model strip not whole rows");
     for (int t = t_hi - 1; t >= t_lo; --t) {
-        st = solve_layer(M, ptab, t, 0, M->ny, values, policy, s);
+        st = solve_layer(M, ptab, t, M->cell0 / M->nx, (M->cell0 + M->ncell) / M->nx, values, policy, s);
         if (st != FM_OK) return st;
     }
     FM_CK(cudaFreeAsync(ptab, s));

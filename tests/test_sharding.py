@@ -113,3 +113,37 @@ def test_sharded_backward_solve_gloo(tmp_path, case, world):
     got = sum(np.load(f"{out}.{r}.npy") for r in range(world))
     assert res == 0.0
     assert got.tobytes() == ref_v.tobytes()
+
+
+def test_weighted_strips_balance_obstacle_cost():
+    """Rows near obstacles cost more (per-transition build path): the
+    obstacle band's strip gets fewer rows; strips stay contiguous and cover
+    every row."""
+    from paper_2109_00857_b200.sharding import row_costs, weighted_strips
+    env, acts, rcfg, target, _ = make_named_env("desk")
+    mask = env.obstacles.mask
+    costs = row_costs(mask, 7, 9)
+    assert costs.shape == (env.grid.ny,) and (costs >= env.grid.nt * env.grid.nx).all()
+    for world in (1, 2, 3, 4, 8):
+        b = weighted_strips(costs, world)
+        assert b[0][0] == 0 and b[-1][1] == env.grid.ny
+        assert all(x1 == y0 for (_, x1), (y0, _) in zip(b, b[1:])) and all(a < c for a, c in b)
+        per = [costs[a:c].sum() for a, c in b]
+        assert max(per) - min(per) <= costs.max() + 1e-9   # balanced up to one row
+    # uniform costs give the equal strips
+    assert weighted_strips(np.ones(10), 3) == [strip_bounds(10, 3, r) for r in range(3)] or \
+        sorted(c - a for a, c in weighted_strips(np.ones(10), 3)) == [3, 3, 4]
+
+
+def test_halo_plan_with_uneven_bounds():
+    bounds = [(0, 2), (2, 9), (9, 10), (10, 20)]
+    for hy in (1, 3, 6):
+        plans = [halo_plan(20, 4, r, hy, bounds) for r in range(4)]
+        for r, (sends, recvs) in enumerate(plans):
+            j0, j1 = bounds[r]
+            need = set(range(max(0, j0 - hy), min(20, j1 + hy))) - set(range(j0, j1))
+            got = set()
+            for peer, a, b in recvs:
+                got |= set(range(a, b))
+                assert (r, a, b) in plans[peer][0]   # the peer sends exactly these rows
+            assert got == need

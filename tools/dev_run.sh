@@ -1,10 +1,9 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/sanitizer
-timeout 300 python tools/sanitize_cases.py > gpurun_out/sanitizer/plain.log 2>&1; echo plain rc=$?; tail -8 gpurun_out/sanitizer/plain.log
-for tool in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize_cases.py > gpurun_out/sanitizer/$tool.log 2>&1; echo $tool rc=$?; tail -4 gpurun_out/sanitizer/$tool.log
-done
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?; tail -3 gpurun_out/bench.err
 python -c "
 import json; d=json.loads(open('gpurun_out/bench.json').read().strip().splitlines()[-1])
-print({k: d[k] for k in ('value','ms_per_step','stages','clocks')}); print(d['e2e']['ms_per_step'], d['roofline']['frac'], d['cpu_baseline']['value'])"
+print({k: d[k] for k in ('value','ms_per_step','stages','clocks','gpu_launches')}); print('e2e', d['e2e']['ms_per_step'], 'dropin', d['e2e_dropin']['ms_per_step'], d['roofline'], d['issue_roofline'])"
+timeout 600 python bench.py --gpus 3 --dist-backend gloo --steps 2 --warmup 1 --workload desk > gpurun_out/bench_gloo3.json 2> gpurun_out/bench_gloo3.err; echo gloo3 rc=$?
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_gloo3.json').read().strip().splitlines()[-1])
+print({k: d[k] for k in ('n_gpus','value','ms_per_step','stages')})"
