@@ -55,6 +55,11 @@ def _args():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default=WORKLOAD)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--reserve-sms", type=int, default=2,
+                   help="SMs the build leaves to the pipelined solve stream (with --groups > 1)")
+    p.add_argument("--groups", type=int, default=5,
+                   help="slab groups per build: the solve of a group (and its halo exchange) and the model's "
+                        "D2H start while the next group builds")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo: validation of the N>1 path with several ranks on one GPU (halo and maxima "
                         "staged through host memory); never a bench number")
@@ -258,8 +263,8 @@ def run_ours(args):
     # N > 1 the build runs in 5 descending slab groups with the per-layer
     # solve + halo exchange of each group pipelined on a second stream
     denv = DeviceEnv.from_host(env)
-    planner = StripPlanner(denv, acts, rcfg, w.target, w.buffer, n_groups=5 if world > 1 else 1,
-                           reserve_sms=2 if world > 1 else 0)
+    planner = StripPlanner(denv, acts, rcfg, w.target, w.buffer, n_groups=args.groups,
+                           reserve_sms=args.reserve_sms if args.groups > 1 else 0)
     j0, j1 = planner.j0, planner.j1
     n_g = g.nx * g.ny * g.nt
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -295,6 +300,8 @@ def run_ours(args):
         ms_per_step = total_ms / args.steps
         value = w.transitions / (ms_per_step / 1e3)
         build_ms = statistics.median(e["start"].elapsed_time(e["built"]) for e in stages)
+        scan_ms = statistics.median(e["start"].elapsed_time(e["scanned"]) for e in stages)
+        kbuild_ms = statistics.median(e["scanned"].elapsed_time(e["built"]) for e in stages)
         solve_ms = statistics.median(e["built"].elapsed_time(e["solved"]) for e in stages)
         nnz_rank = stages[-1]["nnz"]
 
@@ -320,11 +327,8 @@ def run_ours(args):
         # model plus value function and policy out"): this rank's row
         # pointers, entry counts, rewards (strip-local, contiguous) and its
         # entries, on a copy stream that overlaps the solve
-        mdl = planner.dm
-        host_m = {"row_ptr": torch.empty_like(mdl.row_ptr, device="cpu").pin_memory(),
-                  "row_nnz": torch.empty_like(mdl.row_nnz, device="cpu").pin_memory(),
-                  "reward": torch.empty_like(mdl.reward, device="cpu").pin_memory(),
-                  "entries": torch.empty(int(mdl.entries.numel()), dtype=torch.int32).pin_memory()}
+        # streamed group by group while the build runs (DeviceModel.stream_to_host)
+        host_m = planner.dm.host_buffers()
         d2h_stream = torch.cuda.Stream()
         e2e_times, d2h_counts = [], []
         for it in range(args.warmup + args.steps):
@@ -336,17 +340,10 @@ def run_ours(args):
             # upload in time slabs, the exact sub-grid scan of each slab
             # overlapping the next slab's copy (the planner's host-input path)
             de = DeviceEnv.from_host_scanned(_HostEnv, j_range=(j0, j1) if world > 1 else None)
-            dm = step(de, scanned=True)
-            d2h_stream.wait_event(stages[-1]["built"])
-            nbytes = 0
-            with torch.cuda.stream(d2h_stream):
-                for k in ("row_ptr", "row_nnz", "reward"):
-                    host_m[k].copy_(getattr(dm, k), non_blocking=True)
-                    nbytes += getattr(dm, k).numel() * getattr(dm, k).element_size()
-                if host_m["entries"].numel() < dm.nnz:   # a capacity retry grew the model
-                    host_m["entries"] = torch.empty(int(dm.entries.numel()), dtype=torch.int32).pin_memory()
-                host_m["entries"][: dm.nnz].copy_(dm.entries[: dm.nnz], non_blocking=True)
-                nbytes += dm.nnz * 4
+            planner.denv = de
+            dm = planner.step(scanned=True, sink=host_m, sink_stream=d2h_stream)
+            stages.append(dict(planner.events, nnz=dm.nnz))
+            nbytes = planner.sink_bytes
             lo, hi = j0 * g.nx, j1 * g.nx
             if world == 1:
                 host_v.copy_(planner.values, non_blocking=True)
@@ -398,30 +395,34 @@ def run_ours(args):
                   "jacobi_iterations": pv.iterations_run, "residual": pv.residual}
 
     # ---- roofline of the dominant kernel (k_build) ------------------------------
-    # The build bins each (cell, realization) once: its
-    # algorithmic work is the f32 reconstruction (2 N_m FMA per velocity
-    # component) plus the floor / fraction / bucket arithmetic (4 ops per
-    # component) -- 4 N_m + 8 FP32 flops per (cell, realization) -- against
-    # the FP32 FMA peak; the kernel is issue-bound (integer binning, shared-
-    # memory counters), so the ncu issue-slot figure is reported beside it.
+    # algorithmic work F = 13 + 4 N_m / |A| flops per
+    # transition (the reference's per-transition arithmetic), achieved =
+    # U F / t_build, against the peak of the pipe the build actually uses --
+    # "FP32 if the filtered FP32 path is adopted" (the binned build: one f32
+    # reconstruction + bucket per (cell, realization), exact f64 only for the
+    # realizations near a landing step).  t_build = the k_build launches alone
+    # (CUDA events between the scan and the end of the build, on the stream
+    # the kernels run on).  The executed f32 work and the issue-slot use of
+    # the same launches are reported beside it.
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     f_clk = (clocks["sm_mhz"] or 1965.0) * 1e6
     cells_rank = (j1 - j0) * g.nx
+    units_rank = cells_rank * g.nt * w.n_actions * w.n_realizations
+    F = 13 + 4 * w.n_modes / w.n_actions
+    achieved = units_rank * F / (kbuild_ms / 1e3)
+    fp32_peak = sm_count * 128 * 2 * f_clk
     cell_real = cells_rank * g.nt * w.n_realizations
     flops_cr = 4 * w.n_modes + 8
-    achieved = cell_real * flops_cr / (build_ms / 1e3)
-    fp32_peak = sm_count * 128 * 2 * f_clk
     prof = _load_json(os.path.join(ROOT, "profiles", "r02_k_build_paper_ncu.json")) or {}
     traffic = prof.get("dram_bytes_build") if args.workload == WORKLOAD else None
     issue = None
     if prof.get("warp_instructions_build") and args.workload == WORKLOAD and world == 1:
-        ach_i = prof["warp_instructions_build"] / (build_ms / 1e3)
+        ach_i = prof["warp_instructions_build"] / (kbuild_ms / 1e3)
         issue = {"achieved": ach_i / 1e12, "peak": sm_count * 4 * f_clk / 1e12, "unit": "Twarp-instr/s",
                  "frac": ach_i / (sm_count * 4 * f_clk),
                  "note": "ncu executed warp instructions of one build (profiles/r02_k_build_paper_ncu.json) / "
-                         "this run's build time, against 4 issue slots per SM per clock"}
+                         "this run's k_build time, against 4 issue slots per SM per clock"}
     fp64_ceiling = sm_count * 64 * f_clk
-    ref_flops = (13 + 4 * w.n_modes / w.n_actions) * cells_rank * g.nt * w.n_actions * w.n_realizations
 
     # backward solve against HBM: 12 B per entry (4 B column
     # + 8 B probability), 8 B reward per (state, action) row, 18 B per state
@@ -439,33 +440,35 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(w, world, args.dist_backend),
-            "stages": {"scan_build_ms_median": build_ms, "solve_exposed_ms_median": solve_ms,
+            "stages": {"scan_build_ms_median": build_ms, "scan_ms_median": scan_ms, "k_build_ms_median": kbuild_ms, "solve_exposed_ms_median": solve_ms,
                        "step_ms": ms_per_step, "nnz_rank0": nnz_rank, "strips": planner.bounds,
                        "pipelined_slab_groups": planner.n_groups},
             "e2e": {"value": e2e_value, "unit": "transitions/s", "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h_total, "ms_per_step": e2e_ms / args.steps,
                     "path": "pinned host inputs -> DeviceEnv.from_host_scanned (slab-wise H2D + exact scan) -> "
-                            "build -> backward solve -> D2H of values, policy and the compact model (row_ptr, "
-                            "row_nnz, reward, entries)"},
+                            "build in slab groups -> backward solve -> D2H of values, policy and the compact model "
+                            "(row_ptr, row_nnz, reward, entries; streamed per slab group while later groups "
+                            "build: DeviceModel.stream_to_host)"},
             "e2e_dropin": dropin,
             "roofline": {"bound": "fp32", "kernel": "k_build", "achieved": achieved / 1e12,
                          "peak": fp32_peak / 1e12, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-                         "traffic": traffic,
-                         "peak_source": f"{sm_count} SMs x 128 FP32 lanes x 2 (FMA) x the median SM clock under load",
-                         "flops_per_cell_realization": flops_cr,
-                         "flops_note": "per (cell, realization): 2 N_m FMA per velocity component (f32 "
-                                       "reconstruction) + floor/frac/bucket (4 ops per component); the build "
-                                       "also spends integer binning and one shared-memory increment per "
-                                       "(cell, realization) -- it is issue-bound, see issue_roofline",
-                         "time_includes": "exact sub-grid scan (k_vmax) + build (all launches) of this rank"},
+                         "traffic": traffic, "ms_per_launch_set": kbuild_ms,
+                         "flops_per_transition": F, "units_per_step": units_rank,
+                         "peak_source": f"{sm_count} SMs x 128 FP32 lanes x 2 (FMA) x the median SM clock under "
+                                        "load (no FP32 figure in MEASURED_PEAKS.json)",
+                         "definition": "SURVEY.md 8(d): U x F / t_build, F = 13 + 4 N_m/|A| algorithmic flops per "
+                                       "transition, P = the pipe the build uses (FP32: the filtered binned path)",
+                         "traffic_note": "dram__bytes_read+write of the k_build launches of one build (ncu --set "
+                                         "full), vs 185 MB of inputs + the emitted model"},
+            "executed_roofline": {
+                "achieved": cell_real * flops_cr / (kbuild_ms / 1e3) / 1e12, "peak": fp32_peak / 1e12,
+                "unit": "TFLOP/s", "frac": cell_real * flops_cr / (kbuild_ms / 1e3) / fp32_peak,
+                "flops_per_cell_realization": flops_cr,
+                "note": "the f32 work the binned build executes: per (cell, realization) 2 N_m FMA per velocity "
+                        "component + floor/frac/bucket (4 ops per component); the rest of its instructions are "
+                        "integer binning and shared-memory counters -- see issue_roofline"},
             "issue_roofline": issue,
-            "reference_flops_equivalent": {
-                "flops_per_transition": 13 + 4 * w.n_modes / w.n_actions,
-                "achieved": ref_flops / (build_ms / 1e3) / 1e12, "unit": "TFLOP/s",
-                "fp64_issue_ceiling": fp64_ceiling / 1e12,
-                "note": "SURVEY.md 8(d)'s per-transition FP64 count of the reference's algorithm, over this "
-                        "build's time: the binned build does one f32 pass per (cell, realization) instead of "
-                        "per (cell, action, realization), so this exceeds the FP64 ceiling"},
+            "fp64_issue_ceiling_tflops": fp64_ceiling / 1e12,
             "solve_roofline": {"bound": "hbm", "kernel": "k_solve_layer (backward sweep, nt launches)",
                                "achieved": solve_bytes / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else None,
                                "peak": hbm_peak, "unit": "GB/s",

@@ -407,6 +407,64 @@ class DeviceModel:
     _pending: tuple | None = None
     _scratch: tuple | None = None
     group_events: list = field(default_factory=list)   # ((t0, t1), cuda event) per launch group
+    group_nnz: object = None   # pinned int64 [groups]: the entry counter after each group
+
+    def host_buffers(self) -> dict:
+        """Pinned host buffers for stream_to_host / copy_to_host."""
+        torch = _torch()
+        return {"row_ptr": torch.empty(self.row_ptr.numel(), dtype=torch.int64).pin_memory(),
+                "row_nnz": torch.empty(self.row_nnz.numel(), dtype=torch.int16).pin_memory(),
+                "reward": torch.empty(self.reward.numel(), dtype=torch.float64).pin_memory(),
+                "entries": torch.empty(int(self.entries.numel()), dtype=torch.int32).pin_memory()}
+
+    def stream_to_host(self, host: dict, stream) -> int:
+        """Copy the compact model to pinned host buffers while the build is
+        still running: for each slab group (launch order), wait for its
+        build on the host, then queue the D2H of its rows (row pointers,
+        entry counts, rewards: one contiguous range per group) and of the
+        entries it appended (bump-allocated: [counter before, counter
+        after)) on ``stream``.  Without groups: one copy after the build.
+        Returns the bytes copied.  If check() later reports a rebuild
+        (capacity), the caller must copy again (copy_to_host)."""
+        torch = _torch()
+        if not self.group_events or self.group_nnz is None:
+            stream.wait_stream(torch.cuda.current_stream())
+            return self.copy_to_host(host, stream)
+        g, na = self.grid, self.n_actions
+        cap = int(self.entries.numel())
+        prev, nbytes = 0, 0
+        for k, ((g0, g1), ev) in enumerate(self.group_events):
+            ev.synchronize()
+            end = min(int(self.group_nnz[k]), cap)
+            r0, r1 = g0 * self.ncell * na, g1 * self.ncell * na
+            stream.wait_event(ev)
+            with torch.cuda.stream(stream):
+                for key in ("row_ptr", "row_nnz", "reward"):
+                    src = getattr(self, key)[r0:r1]
+                    host[key][r0:r1].copy_(src, non_blocking=True)
+                    nbytes += src.numel() * src.element_size()
+                if end > prev:
+                    host["entries"][prev:end].copy_(self.entries[prev:end], non_blocking=True)
+                    nbytes += (end - prev) * 4
+            prev = max(prev, end)
+        return nbytes
+
+    def copy_to_host(self, host: dict, stream) -> int:
+        """The whole compact model to pinned host buffers on ``stream``
+        (after check()); returns the bytes copied."""
+        torch = _torch()
+        self.check()
+        nbytes = 0
+        with torch.cuda.stream(stream):
+            for key in ("row_ptr", "row_nnz", "reward"):
+                src = getattr(self, key)
+                host[key].copy_(src, non_blocking=True)
+                nbytes += src.numel() * src.element_size()
+            if host["entries"].numel() < self.nnz:
+                host["entries"] = torch.empty(int(self.entries.numel()), dtype=torch.int32).pin_memory()
+            host["entries"][: self.nnz].copy_(self.entries[: self.nnz], non_blocking=True)
+            nbytes += self.nnz * 4
+        return nbytes
 
     def check(self) -> bool:
         """Finish a (deferred) build: census, sub-grid overflow (raises the
@@ -600,10 +658,17 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
     if t_groups:
         if sorted(t for g in t_groups for t in range(*g)) != list(range(t0, t1)):
             raise ContractViolation("t_groups must partition the slab range")
-        for g0, g1 in t_groups:
+        # the entry counter after each group, copied to pinned host memory
+        # in stream order (stream_to_host reads it once the group's event fired)
+        snap = getattr(reuse, "group_nnz", None) if reuse is not None else None
+        if snap is None or snap.numel() < len(t_groups):
+            snap = torch.zeros(len(t_groups), dtype=torch.int64).pin_memory()
+        dm.group_nnz = snap
+        for k, (g0, g1) in enumerate(t_groups):
             ga = _lib.FmBuildArgs.from_buffer_copy(args)
             ga.t0, ga.t1 = int(g0), int(g1)
             _lib.check(L.fm_build_launch(C.byref(ga), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
+            snap[k:k + 1].copy_(d_nnz, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
             dm.group_events.append(((int(g0), int(g1)), ev))

@@ -103,9 +103,32 @@ static int sm_count()
 #ifdef FM_STATS
 __device__ unsigned long long g_fm_stats[8];
 #define FM_STAT(i, n) atomicAdd(&g_fm_stats[i], (unsigned long long)(n))
+// per-task cycle counts of PART-2 launches (dev: task id << 40 | path << 36 | cycles)
+__device__ unsigned long long g_fm_ttimes[1 << 20];
+__device__ unsigned int g_fm_tcount;
+// per-warp counters of the current task (dev): [warp][0] D items, [1] gated items, [2] pairs, [3] seg tests
+__device__ unsigned int g_fm_wcnt[148 * 64][8];   // + [4] init cycles/64, [5] drain cycles/64, [6] loop+drain cycles/64
 #else
 #define FM_STAT(i, n) ((void)0)
 #endif
+extern "C" int32_t fm_dev_task_times(uint64_t *h_out, int32_t max_n, int32_t *h_n)
+{
+#ifdef FM_STATS
+    unsigned int n = 0;
+    FM_CK(cudaMemcpyFromSymbol(&n, g_fm_tcount, 4));
+    if (n > (unsigned)max_n) n = (unsigned)max_n;
+    if (n > (1u << 17)) n = 1u << 17;
+    FM_CK(cudaMemcpyFromSymbol(h_out, g_fm_ttimes, 8ull << 20));
+    *h_n = (int32_t)n;
+    const unsigned int z = 0;
+    FM_CK(cudaMemcpyToSymbol(g_fm_tcount, &z, 4));
+    return FM_OK;
+#else
+    (void)h_out; (void)max_n;
+    *h_n = 0;
+    return FM_OK;
+#endif
+}
 extern "C" int32_t fm_dev_stats(uint64_t *h_out8)
 {
 #ifdef FM_STATS
@@ -644,10 +667,15 @@ enum : int { RF_DEAD = 1, RF_TERMINAL = 2, RF_GATE = 4, RF_LANDWIN = 8, RF_SEGWI
 // error bound; a realization closer than the zone half-width to any step
 // (or with any doubt) takes the exact f64 path of the reference instead
 // (bin_drain), so the counts equal the reference's bit for bit.
-static constexpr int kBinNS = 128;    // buckets per unit interval of frac(z)
+static constexpr int kBinNS = 128;    // max buckets per unit interval of frac(z) (bin_ns: 32, 64 or 128)
+static constexpr int kBinRep = 16;    // block-shared copies of each table entry (conflict-free lookups)
 static constexpr int kBinMaxA = 64;   // actions with bin parameters
 static constexpr int kBinRing = 8;    // coefficient chunks in flight (32 realizations each)
 static constexpr int kBinQ = 128;     // deferred exact realizations per warp
+// obstacle tasks (bin_task<.., OB = true>): a smaller ring beside (not under)
+// the dense histogram, and a larger queue drained whenever it fills up
+static constexpr int kBinRingO = 4;
+static constexpr int kBinQO = 256;
 struct BinEnt {
     // the zone intersecting the bucket: frac in [lo, hi] -> exact path; the
     // low 6 mantissa bits of lo hold kb + 1, kb = the sub-bin below the zone
@@ -661,7 +689,7 @@ struct BinAct {
 struct BuildK {
     // grid
     int nx, ny, nt, nc;
-    double dx, dt, ox, oy, inv_dx, half_dx;
+    double dx, dt, ox, oy, inv_dx, half_dx, inv_half_dx;
     // env
     const double *mean, *modes, *coeffs, *g;
     const uint8_t *mask;
@@ -699,6 +727,7 @@ struct BuildK {
     unsigned long long *nnz_counter;
     uint32_t *viol;
     unsigned int *task_counter;
+    unsigned int *task_list, *task_list_n;   // tasks the bin-only launches could not bin (PART 0 list launch)
     uint16_t *ghist;   // F_GHIST: [resident warp][nslot + 1][32]
     // ---- per-(cell, realization) binning of lean tasks (see bin_task) ----
     int bin_ok;                 // the launch has bin tables (PART 1 lean tasks use them)
@@ -712,10 +741,14 @@ struct BuildK {
     int off_block;              // block-shared bytes before the warps' regions (bin tables)
     int off_bins, off_bdense, off_bq;   // per-warp regions of the bin path (union with the legacy ones):
                                         // counters | coefficient ring, later the dense histogram | queue
-    const float *coef32;        // [t - t0][nr][8] f32 coefficients (zero padded), per launch
+    int off_bring;                      // the coefficient ring (= off_bdense for lean tasks; separate for
+                                        // obstacle tasks, which drain into the dense histogram mid-loop)
+    const float *coef32;        // [t - t0][nr_pad][8] f32 coefficients (zero padded), per launch
+    int nr_pad;                 // realizations rounded up to a multiple of 128
     const double *cmax;         // [t - t0][nm] max_r |coeff[t, r, m]|
     const int4 *envelope;       // [nt][nc] per-cell velocity envelope (fm_velocity_scan) or null
-    BinEnt tab[2 * (kBinNS + 1)];   // bucket tables, x then y (entry NS: frac == 1)
+    int bin_ns;                 // buckets per unit of frac(z): the smallest of 32 / 64 / 128 giving the same zones
+    BinEnt tab[2 * (kBinNS + 1)];   // bucket tables, x then y, stride kBinNS + 1 (entry NS: frac == 1)
     BinAct bact[kBinMaxA];      // per action: (gamma_x, cluster r_x, gamma_y, r_y)
 };
 
@@ -749,6 +782,13 @@ __device__ __forceinline__ int box_count(const BuildK &K, int t, int i0, int i1,
     const int W = K.nx + 1;
     const int32_t *S = K.sat + (size_t)t * W * (K.ny + 1);
     return S[(j1 + 1) * W + i1 + 1] - S[j0 * W + i1 + 1] - S[(j1 + 1) * W + i0] + S[j0 * W + i0];
+}
+
+// floor(u) for |u| < 2^31 by one round-down add of 1.5 * 2^52 (the F2I
+// conversion runs on the XU pipe at a quarter of the FP64 rate)
+__device__ __forceinline__ int floor_magic(double u)
+{
+    return __double2loint(__dadd_rd(u, 6755399441055744.0));
 }
 
 // (x - origin) / dx with the reference's rounding (model_builder.py:333-334);
@@ -819,6 +859,58 @@ __device__ __forceinline__ bool seg_samples_blocked(const BuildK &K, int t, doub
         const long long i = __double2ll_rd(to_cell<FLAGS>(px, K.ox, K.dx, K.inv_dx));
         const long long j = __double2ll_rd(to_cell<FLAGS>(py, K.oy, K.dx, K.inv_dx));
         if (i >= 0 && i < K.nx && j >= 0 && j < K.ny && __ldg(mt + j * K.nx + i)) return true;
+    }
+    return false;
+}
+
+// seg_samples_blocked for an obstacle bin task: the segment-sampling
+// fractions fl(q / n) for n <= kFracSmemN from a block-shared copy of the
+// table, and the mask at t from a per-cell shared window of cells
+// [ci - hx - 1, ci + hx + 1] x [cj - hy - 1, cj + hy + 1] (every sample of a
+// landing inside the sub-grid window lies in it: the samples are monotone
+// between x0 and the transit end, which is within one cell of the landing);
+// anything outside falls back to global memory.  Same arithmetic as
+// environment.py:353-367.
+static constexpr int kFracSmemN = 16;
+template <int FLAGS>
+__device__ __forceinline__ bool seg_samples_blocked_win(const BuildK &K, const double *ftab_s, const uint8_t *mwin,
+                                                        int wi0, int wj0, int ww, int wh, int t, double p0x,
+                                                        double p0y, double p1x, double p1y)
+{
+    const double ddx = DSUB(p1x, p0x), ddy = DSUB(p1y, p0y);
+    const double len = fm_hypot(ddx, ddy);
+    // ceil(len / (0.5 dx)): for a power-of-two dx the quotient is an exact
+    // scaling, so the product by the reciprocal rounds identically
+    double ns = ceil((FLAGS & (F_DX_ONE | F_DX_MUL)) ? DMUL(len, K.inv_half_dx) : DDIV(len, K.half_dx));
+    if (!(ns >= 1.0)) ns = 1.0;
+    const long long n = (long long)ns;
+    FM_STAT(1, 1);
+    FM_STAT(2, n + 1);
+    const uint8_t *mt = K.mask + (size_t)t * K.nc;
+    const double *ftab = n <= kFracSmemN ? ftab_s + n * (n + 1) / 2 : n <= kFracMaxN ? g_frac + n * (n + 1) / 2 : nullptr;
+    // four independent samples per step (early exit per step); coordinates
+    // are below 2^30 cells (F_PROVEN), so floor is one round-down add
+    for (long long q0 = 0; q0 <= n; q0 += 4) {
+        bool hit = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long q = q0 + u;
+            if (q <= n) {
+                double frac = ftab ? ftab[q] : DDIV((double)q, ns);
+                if (frac > 1.0) frac = 1.0;
+                const double px = DADD(p0x, DMUL(frac, ddx));
+                const double py = DADD(p0y, DMUL(frac, ddy));
+                const int i = floor_magic(to_cell<FLAGS>(px, K.ox, K.dx, K.inv_dx));
+                const int j = floor_magic(to_cell<FLAGS>(py, K.oy, K.dx, K.inv_dx));
+                if ((unsigned)i < (unsigned)K.nx && (unsigned)j < (unsigned)K.ny) {
+                    const int li = i - wi0, lj = j - wj0;
+                    hit |= ((unsigned)li < (unsigned)ww && (unsigned)lj < (unsigned)wh)
+                               ? mwin[lj * ww + li] != 0
+                               : __ldg(mt + j * K.nx + i) != 0;
+                }
+            }
+        }
+        if (hit) return true;
     }
     return false;
 }
@@ -973,10 +1065,6 @@ __device__ __noinline__ SlowOut rare_transition(const BuildK *__restrict__ Kg, i
 // is 1, so the round-down add is exactly 1.5*2^52 + floor(u); its low word
 // is floor(u) in two's complement.  One DADD instead of an F2I (XU pipe,
 // a quarter of the FP64 rate).
-__device__ __forceinline__ int floor_magic(double u)
-{
-    return __double2loint(__dadd_rd(u, 6755399441055744.0));
-}
 
 // Branch-free fast transition.  Valid when the landing is inside the row's
 // grid-clipped window and (OBST) not on a danger slot of the row's cell --
@@ -1487,6 +1575,12 @@ __device__ __forceinline__ float2 f2_add_rm(float2 a, float2 b)
     asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
     return f2_from(r);
 }
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b)
+{
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(r);
+}
 __device__ __forceinline__ float2 f2_sub(float2 a, float2 b)
 {
     unsigned long long r;
@@ -1583,10 +1677,11 @@ __device__ __forceinline__ double2 exact_velocity(const BuildK &K, int t, int r,
     return make_double2(vx, vy);
 }
 
-// Deferred realizations (within a zone, or out of the box): the exact f64
-// velocity, then every row of its cell takes the reference's transition
-// (lean_transition, as the per-transition path) into the dense histogram.
-// Items are (cell slot << 16 | r); the last n <= 32 are processed.
+// Deferred realizations of a lean bin task (within a zone, or out of the
+// box): the exact f64 velocity, then every row of its cell takes the
+// reference's transition (lean_transition, as the per-transition path) into
+// the dense histogram.  Items are (cell slot << 16 | r); the last n <= 32
+// are processed.
 template <int FLAGS>
 __device__ __forceinline__ int bin_drain(const BuildK &K, const uint32_t *bq, int qn, int t, int grp,
                                          const RowC &Rf, uint16_t *h16q, unsigned hs_word, int outq, bool row_ok,
@@ -1615,194 +1710,492 @@ __device__ __forceinline__ int bin_drain(const BuildK &K, const uint32_t *bq, in
     return first;
 }
 
+// Obstacle bin tasks: queue items are (r | cell slot << 16 | kind), kind =
+// bit 17 (a doubtful realization: not binned, every live row takes the
+// exact transition) or the bin index << 18 (a binned realization whose bin
+// marks, in its high half, the rows landing on a danger class 2 / 3 slot:
+// those rows take the exact transit test and move the transition to OUT
+// when it is blocked).  The work is spread over the warp per (item, row)
+// pair; every dense-histogram update is a 32-bit shared-memory add on the
+// word holding the owner row's u16 counter (+-1 << 16 * (owner & 1)), so
+// the pairs' +-1 and the epilogue's rectangle sums commute modulo 2^32 and
+// the final halves are exact (each true count lies in [0, 65535]).
+// environment.py:338-368 (transit test), model_builder.py:331-347 (landing).
+static constexpr uint32_t kItemD = 1u << 17;
+struct ObstDrainBuf {
+    double2 v[32];
+    int32_t scan[32];
+    uint32_t mask[32];
+    uint32_t meta[32];
+    // per task: the cells' centres (environment.py:99-100), columns / rows,
+    // window offsets, and the task's action vectors
+    double2 x0[2];
+    int32_t ci[2], cj[2], soff[2], pad_[2];
+    double2 act[32];
+};
+
+template <int FLAGS>
+__device__ __noinline__ int bin_drain_obst(const BuildK &K, const uint32_t *bq, const uint32_t *bins, int qn, int t,
+                                              int grp, int ag, unsigned dense_s, const uint32_t *danger, int CWD,
+                                              ObstDrainBuf *db, const double *ftab_s, const uint8_t *mwin)
+{
+    const int ww = 2 * K.hx + 3, wh = 2 * K.hy + 3;
+    const int lane = threadIdx.x & 31;
+    const int n = qn < 32 ? qn : 32, first = qn - n;
+    if (lane == 0) FM_STAT(6, n);
+    const int AG = K.AG;
+    const int na_loc = min(AG, K.na - ag * 32);
+    int cnt = 0;
+#ifdef FM_STATS
+    const unsigned gw = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % (148 * 64);
+    if (lane < n) atomicAdd(&g_fm_wcnt[gw][(bq[first + lane] & kItemD) ? 0 : 1], 1u);
+#endif
+    if (lane < n) {
+        const uint32_t it = bq[first + lane];
+        const int cs = (int)((it >> 16) & 1u);
+        const int r = (int)(it & 0xFFFFu);
+        db->v[lane] = exact_velocity(K, t, r, K.cell0 + grp * K.CW + cs);
+        const uint32_t m = (it & kItemD) ? (na_loc >= 32 ? 0xFFFFFFFFu : (1u << na_loc) - 1u) : (bins[it >> 18] >> 16);
+        db->mask[lane] = m;
+        db->meta[lane] = it;
+        cnt = __popc(m);
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    db->scan[lane] = incl;
+    const int total = __shfl_sync(kFull, incl, 31);
+    __syncwarp();
+#ifdef FM_STATS
+    const long long cp0 = clock64();
+#endif
+    for (int k = lane; k < total; k += 32) {
+        // item e: the first with scan[e] > k; row: the j-th set bit of its mask
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (db->scan[mid] > k) hi = mid;
+            else lo = mid + 1;
+        }
+        const int e = lo;
+        const int j = k - (e ? db->scan[e - 1] : 0);
+        unsigned al;
+        asm("fns.b32 %0, %1, 0, %2;" : "=r"(al) : "r"(db->mask[e]), "r"(j + 1));
+        const uint32_t it = db->meta[e];
+        const int cs = (int)((it >> 16) & 1u);
+        const int owner = cs * AG + (int)al;
+        // the row's constants (model_builder.py:331-335), staged per task
+        RowC R;
+        R.ci = db->ci[cs];
+        R.cj = db->cj[cs];
+        R.x0 = db->x0[cs].x;
+        R.y0 = db->x0[cs].y;
+        R.ax = db->act[al].x;
+        R.ay = db->act[al].y;
+        R.soff = db->soff[cs];
+        const uint32_t *cls = danger + cs * CWD;
+        const double2 v = db->v[e];
+        double px = DADD(v.x, R.ax), py = DADD(v.y, R.ay);   // x' = x0 + (v + a) * dt
+        if (!(FLAGS & F_DT_ONE)) {
+            px = DMUL(px, K.dt);
+            py = DMUL(py, K.dt);
+        }
+        const double x1 = DADD(R.x0, px), y1 = DADD(R.y0, py);
+        const int i1 = floor_magic(to_cell<FLAGS>(x1, K.ox, K.dx, K.inv_dx));
+        const int j1 = floor_magic(to_cell<FLAGS>(y1, K.oy, K.dx, K.inv_dx));
+        const int slot = j1 * K.width + i1 + R.soff;   // inside the window (F_PROVEN)
+        const int cl = (int)((cls[slot >> 4] >> ((slot & 15) << 1)) & 3u);
+#ifdef FM_STATS
+        atomicAdd(&g_fm_wcnt[gw][2], 1u);
+        if (cl >= 2) atomicAdd(&g_fm_wcnt[gw][3], 1u);
+#endif
+        const bool blocked = cl >= 2 && seg_samples_blocked_win<FLAGS>(K, ftab_s, mwin + cs * ww * wh,
+                                                                      R.ci - K.hx - 1, R.cj - K.hy - 1, ww, wh, t,
+                                                                      R.x0, R.y0, x1, y1);
+        const unsigned sh = (unsigned)(owner & 1) * 16u;
+        const unsigned wofs = (unsigned)(owner >> 1) * 4u;
+        const unsigned w_slot = dense_s + (unsigned)slot * 64u + wofs;
+        const unsigned w_out = dense_s + (unsigned)K.nslot * 64u + wofs;
+        if (it & kItemD) {   // not binned: the whole transition here
+            const unsigned w = (cl == 1 || blocked) ? w_out : w_slot;
+            asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(w), "r"(1u << sh) : "memory");
+        } else if (blocked) {   // binned in its landing slot: move it to OUT
+            asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(w_slot), "r"(0u - (1u << sh)) : "memory");
+            asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(w_out), "r"(1u << sh) : "memory");
+        }
+    }
+    __syncwarp();
+#ifdef FM_STATS
+    if (lane == 0) g_fm_wcnt[gw][7] += (unsigned)((clock64() - cp0) >> 6);
+#endif
+    return first;
+}
+
 // The realization loop of one bin task over NC (1 or 2) cells: f32
 // reconstruction, bin, one shared-memory increment per (cell, realization);
 // realizations with any doubt are queued for the exact path.  Coefficients
-// stream through a per-warp ring of 32-realization chunks (cp.async, kBinRing
-// chunks in flight), two chunks per iteration.  Returns the queue length, or
-// -1 when the queue overflowed (the task then takes the per-transition path).
-template <int NC>
-__device__ __forceinline__ int bin_loop(const BuildK &K, const BinCell *B, int p, int t, const BinEnt *tab_s,
-                                        unsigned bins_s, unsigned ring_s, uint32_t *bq)
+// stream through a per-warp ring of 32-realization chunks (cp.async, RING
+// chunks in flight), two chunks per iteration.  Lean tasks (OB = false):
+// returns the queue length, or -1 when the queue overflowed (the task then
+// takes the per-transition path).  Obstacle tasks (OB = true): a bin's high
+// half holds the mask of the rows whose landing from it lies on a danger
+// class 2 / 3 slot (set by bin_task); a realization binned there is counted
+// and also queued (the atomic returns the bin's old value), and the queue
+// is drained (`drain`, bin_drain_obst) whenever the next iteration could
+// overflow it.
+#ifndef FM_BIN_H
+#define FM_BIN_H 2
+#endif
+template <int NC, bool OB, int RING, typename Drain>
+__device__ __forceinline__ int bin_loop(const BuildK &K, const BinCell *B, const int *cid, bool two, int t,
+                                        const BinEnt *tab_s, unsigned bins_s, unsigned ring_s, uint32_t *bq,
+                                        Drain &&drain)
 {
     const int lane = threadIdx.x & 31, nr = K.nr;
-    const int nch = (nr + 31) >> 5;
-    const float2 ip2 = make_float2(K.bin_ip, K.bin_ip);
+    const int nch = K.nr_pad >> 5;   // a multiple of 4: coefficients zero-padded to 128-realization multiples
+    const float2 ip2 = make_float2(K.bin_ip, K.bin_ip);   // 1 / p (exactly 1 for p = 1)
     const float2 M2 = make_float2(12582912.0f, 12582912.0f);   // 1.5 * 2^23: floor by a round-down add
-    const float2 NS2 = make_float2((float)kBinNS, (float)kBinNS);
-    const unsigned tabx_s = (unsigned)__cvta_generic_to_shared(tab_s) - 0x4B400000u * 8u;   // bucket bits -> entry
-    const unsigned taby_s = tabx_s + (kBinNS + 1) * 8u;
+    const int ns = K.bin_ns;
+    const float2 NS2 = make_float2((float)ns, (float)ns);
+    // bucket bits -> this lane's copy of the table entry ([axis][bucket][copy]
+    // of 8 B: lanes l and l + 16 share a copy, so a lookup is conflict-free):
+    // one opaque base with the bias folded in
+    unsigned tabx_s;
+    asm("mov.b32 %0, %1;"
+        : "=r"(tabx_s)
+        : "r"((unsigned)__cvta_generic_to_shared(tab_s) + 8u * (unsigned)(lane & (kBinRep - 1)) -
+              0x4B400000u * (8u * kBinRep)));
+    const unsigned taby_s = tabx_s + (unsigned)(ns + 1) * (8u * kBinRep);
     const int k1x = K.bin_k1x, k1y = K.bin_k1y;
-    // bin = (bits(M + floor z) - bits(M)) * k1 + kb - off: constants folded
-    unsigned cx[NC], cy[NC];   // modulo 2^32: the products with the bias bits wrap and cancel
-    int bxn[NC], byn[NC];
+    constexpr int QCAP = OB ? kBinQO : kBinQ;
+    // bin = (bits(M + floor z) - bits(M)) * k1 + kb - off, with kb + 1 in the
+    // table entry's low bits: the -1, the bias and the offset fold into one
+    // constant (modulo 2^32: the products with the bias bits wrap and cancel)
+    unsigned cx[NC], cy[NC];
+    unsigned bxn[NC], byn[NC];
     unsigned bb[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
-        cx[q] = 0u - 0x4B400000u * (unsigned)k1x - (unsigned)B[q].offx;
-        cy[q] = 0u - 0x4B400000u * (unsigned)k1y - (unsigned)B[q].offy;
-        bxn[q] = B[q].bx;
-        byn[q] = B[q].by;
+        cx[q] = 0u - 0x4B400000u * (unsigned)k1x - (unsigned)B[q].offx - 1u;
+        cy[q] = 0u - 0x4B400000u * (unsigned)k1y - (unsigned)B[q].offy - 1u;
+        bxn[q] = (unsigned)B[q].bx;
+        byn[q] = (unsigned)B[q].by;
         bb[q] = bins_s + 4u * (unsigned)B[q].base;
     }
-    const char *gsrc = reinterpret_cast<const char *>(K.coef32 + (size_t)(t - K.t0) * nr * 8 + lane * 8);
-    const unsigned rl = ring_s + (unsigned)lane * 32u;
+    // realizations that are not counted (doubtful, or padding) add to a
+    // per-lane dummy counter past the task's bins: no branch per update
+    const unsigned dummy = bins_s + 4u * (unsigned)(K.bin_words - 32 + lane);
+    const char *gsrc = reinterpret_cast<const char *>(K.coef32 + (size_t)(t - K.t0) * K.nr_pad * 8 + lane * 8);
+    // a ring chunk (32 realizations x 8 f32): [coefficients 0-3 of the 32
+    // lanes | coefficients 4-7]: each 16-byte lane read is conflict-free
+    const unsigned rl = ring_s + (unsigned)lane * 16u;
     auto issue = [&](int i) {
-        if (i < nch && i * 32 + lane < nr) {
-            const unsigned d = rl + (unsigned)(i & (kBinRing - 1)) * 1024u;
+        if (i < nch) {
+            const unsigned d = rl + (unsigned)(i & (RING - 1)) * 1024u;
             const char *src = gsrc + (size_t)i * 1024;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 16u), "l"(src + 16) : "memory");
+            // .ca: the warps of an SM sweep the same slab's coefficients
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d + 512u), "l"(src + 16) : "memory");
         }
         cp_async_commit();
     };
 #pragma unroll
-    for (int i = 0; i < kBinRing - 2; ++i) issue(i);
+    for (int i = 0; i < RING - ((RING >= 8) ? FM_BIN_H : 2); ++i) issue(i);
     int qn = 0;
-#ifndef FM_BIN_H
-#define FM_BIN_H 2
-#endif
-    constexpr int H = FM_BIN_H;   // chunks (of 32 realizations) per iteration
-    for (int i = 0; i < nch; i += H) {
-        issue(i + kBinRing - 2);
-        if (H == 2) issue(i + kBinRing - 1);
-        if (H == 2)
-            asm volatile("cp.async.wait_group %0;\n" ::"n"(kBinRing - 2) : "memory");
-        else
-            asm volatile("cp.async.wait_group %0;\n" ::"n"(kBinRing - 3) : "memory");
-        __syncwarp();
-        bool dq[H][NC];
+    constexpr int H = (RING >= 8) ? FM_BIN_H : 2;   // chunks (of 32 realizations) per iteration
+    {
+        for (int i = 0; i < nch; i += H) {
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
-            const int r = (i + h) * 32 + lane;
-            const bool live = r < nr;
-            const unsigned ra = rl + (unsigned)((i + h) & (kBinRing - 1)) * 1024u;
-            float4 c0, c1;
-            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(c0.x), "=f"(c0.y), "=f"(c0.z), "=f"(c0.w) : "r"(ra));
-            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(c1.x), "=f"(c1.y), "=f"(c1.z), "=f"(c1.w) : "r"(ra + 16u));
-            if (!live) {   // past N_rv: stale ring contents must not index the tables
-                c0 = make_float4(0.f, 0.f, 0.f, 0.f);
-                c1 = c0;
+            for (int h = 0; h < H; ++h) issue(i + RING - H + h);
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(RING - H) : "memory");
+            __syncwarp();
+            bool dq[H][NC];
+            uint32_t it_[H][NC];
+            // both chunks' coefficients first (volatile: behind the cp.async
+            // wait, and ahead of every counter update so the two chunks'
+            // chains interleave; the table loads below are plain -- the
+            // tables never change during the loop)
+            float4 c0[H], c1[H];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const unsigned ra = rl + (unsigned)((i + h) & (RING - 1)) * 1024u;
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(c0[h].x), "=f"(c0[h].y), "=f"(c0[h].z), "=f"(c0[h].w) : "r"(ra));
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(c1[h].x), "=f"(c1[h].y), "=f"(c1[h].z), "=f"(c1[h].w) : "r"(ra + 512u));
             }
-            const float cf[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
 #pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                float2 v = B[q].mu;
+            for (int h = 0; h < H; ++h) {
+                const int r = (i + h) * 32 + lane;
+                const bool live_r = r < nr;   // padded realizations (zero coefficients) are binned, never counted
+                const float cf[8] = {c0[h].x, c0[h].y, c0[h].z, c0[h].w, c1[h].x, c1[h].y, c1[h].z, c1[h].w};
 #pragma unroll
-                for (int m = 0; m < 8; ++m) v = ffma2_bcast(cf[m], B[q].md[m], v);
-                const float2 z = K.bin_p1 ? v : f2_mul(v, ip2);
-                const float2 t1 = f2_add_rm(z, M2);             // M + floor(z)
-                const float2 f = f2_sub(z, f2_sub(t1, M2));     // frac(z) in [0, 1] (z finite: F_PROVEN)
-                const float2 tb = f2_fma_rm(f, NS2, M2);        // M + floor(frac * NS), <= M + NS
-                float2 ex, ey;   // (lo | kb + 1 in the low mantissa bits, hi)
-                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(ex.x), "=f"(ex.y) : "r"(tabx_s + 8u * (unsigned)__float_as_int(tb.x)));
-                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(ey.x), "=f"(ey.y) : "r"(taby_s + 8u * (unsigned)__float_as_int(tb.y)));
-                const int kbx = (__float_as_int(ex.x) & 63) - 1, kby = (__float_as_int(ey.x) & 63) - 1;
-                const int bx = (int)((unsigned)__float_as_int(t1.x) * (unsigned)k1x + cx[q] + (unsigned)kbx +
-                                     (f.x > ex.y ? 1u : 0u));
-                const int by = (int)((unsigned)__float_as_int(t1.y) * (unsigned)k1y + cy[q] + (unsigned)kby +
-                                     (f.y > ey.y ? 1u : 0u));
-                // safe: outside this bucket's zone on both axes and inside the box
-                const bool ok = live & ((f.x < ex.x) | (f.x > ex.y)) & ((f.y < ey.x) | (f.y > ey.y)) &
-                                ((unsigned)bx < (unsigned)bxn[q]) & ((unsigned)by < (unsigned)byn[q]);
-                if (ok) asm volatile("red.shared.add.u32 [%0], 1;\n" ::"r"(bb[q] + 4u * (unsigned)(by * bxn[q] + bx)) : "memory");
-                dq[h][q] = live & !ok;
+                for (int q = 0; q < NC; ++q) {
+                    const bool live = live_r && (q == 0 || two);
+                    // (one chain: two interleaved half-chains + an add measured slower)
+                    float2 v = B[q].mu;
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) v = ffma2_bcast(cf[m], B[q].md[m], v);
+                    const float2 z = f2_mul(v, ip2);
+                    const float2 t1 = f2_add_rm(z, M2);             // M + floor(z)
+                    const float2 f = f2_sub(z, f2_sub(t1, M2));     // frac(z) in [0, 1] (z finite: F_PROVEN)
+                    const float2 tb = f2_fma_rm(f, NS2, M2);        // M + floor(frac * NS), <= M + NS
+                    float2 ex, ey;   // (lo | kb + 1 in the low mantissa bits, hi)
+                    asm("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(ex.x), "=f"(ex.y) : "r"(tabx_s + (8u * kBinRep) * (unsigned)__float_as_int(tb.x)));
+                    asm("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(ey.x), "=f"(ey.y) : "r"(taby_s + (8u * kBinRep) * (unsigned)__float_as_int(tb.y)));
+                    // sign bits: f < lo (below the zone), f > hi (above it)
+                    const float2 dlo = f2_sub(f, make_float2(ex.x, ey.x));
+                    const float2 dhi = f2_sub(make_float2(ex.y, ey.y), f);
+                    const unsigned sx = (unsigned)__float_as_int(dhi.x) >> 31, sy = (unsigned)__float_as_int(dhi.y) >> 31;
+                    const unsigned bx = (unsigned)__float_as_int(t1.x) * (unsigned)k1x + cx[q] +
+                                        ((unsigned)__float_as_int(ex.x) & 63u) + sx;
+                    const unsigned by = (unsigned)__float_as_int(t1.y) * (unsigned)k1y + cy[q] +
+                                        ((unsigned)__float_as_int(ey.x) & 63u) + sy;
+                    // safe: outside this bucket's zone on both axes and inside the box
+                    const unsigned zs = ((unsigned)__float_as_int(dlo.x) | (unsigned)__float_as_int(dhi.x)) &
+                                        ((unsigned)__float_as_int(dlo.y) | (unsigned)__float_as_int(dhi.y));
+                    const bool ok = live & ((zs >> 31) != 0u) & (bx < bxn[q]) & (by < byn[q]);
+                    const unsigned widx = by * bxn[q] + bx;
+                    const unsigned addr = ok ? bb[q] + 4u * widx : dummy;
+                    uint32_t item = kItemD;
+                    bool gated = false;
+                    if (OB) {   // counted either way; a bin with a row mask also queues it
+                        unsigned old;
+                        asm volatile("atom.shared.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(addr) : "memory");
+                        gated = ok & ((old >> 16) != 0u);
+                        if (ok) item = (uint32_t)(B[q].base + (int)widx) << 18;
+                    } else {   // no memory clobber: the callers fence before reading the bins
+                        asm volatile("red.shared.add.u32 [%0], 1;\n" ::"r"(addr));
+                    }
+                    dq[h][q] = live & (!ok | gated);
+                    it_[h][q] = item | ((uint32_t)cid[q] << 16) | (uint32_t)r;
+                }
             }
-        }
-        bool any = false;
-#pragma unroll
-        for (int h = 0; h < H; ++h)
-#pragma unroll
-            for (int q = 0; q < NC; ++q) any |= dq[h][q];
-        if (__any_sync(kFull, any)) {
+            bool any = false;
 #pragma unroll
             for (int h = 0; h < H; ++h)
 #pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    const unsigned bm = __ballot_sync(kFull, dq[h][q]);
-                    const int pos = qn + __popc(bm & ((1u << lane) - 1u));
-                    if (dq[h][q] && pos < kBinQ) bq[pos] = ((uint32_t)(p + q) << 16) | (uint32_t)((i + h) * 32 + lane);
-                    qn += __popc(bm);
+                for (int q = 0; q < NC; ++q) any |= dq[h][q];
+            if (__any_sync(kFull, any)) {
+#pragma unroll
+                for (int h = 0; h < H; ++h)
+#pragma unroll
+                    for (int q = 0; q < NC; ++q) {
+                        const unsigned bm = __ballot_sync(kFull, dq[h][q]);
+                        const int pos = qn + __popc(bm & ((1u << lane) - 1u));
+                        if (dq[h][q] && pos < QCAP) bq[pos] = OB ? it_[h][q] : (((uint32_t)cid[q] << 16) | (uint32_t)((i + h) * 32 + lane));
+                        qn += __popc(bm);
+                    }
+                if (OB) {
+                    if (qn > QCAP - H * NC * 32) {   // the next iteration could overflow: drain now
+                        __syncwarp();
+                        drain(qn);
+                        qn = 0;
+                    }
+                } else if (qn > QCAP) {   // too many doubtful realizations: per transition instead
+                    cp_async_wait_all();
+                    __syncwarp();
+                    return -1;
                 }
-            if (qn > kBinQ) {   // too many doubtful realizations: per transition instead
-                cp_async_wait_all();
-                __syncwarp();
-                return -1;
             }
+            __syncwarp();
         }
-        __syncwarp();
     }
     cp_async_wait_all();
     __syncwarp();
     return qn;
 }
 
-// A lean task by binning (see the comment at kBinNS).  Returns false when
-// some cell cannot be binned or too many realizations need the exact path;
-// the caller then runs the per-transition path (which clears its own
-// histogram).  On success the task's dense [slot][row] histogram -- at
-// wbase + off_bdense, over the coefficient ring -- holds exactly the counts
-// the per-transition path would produce.
-template <int FLAGS>
+__device__ __forceinline__ int floordiv_pos(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// A task by binning (see the comment at kBinNS).  Lean tasks (OB = false)
+// and, under F_PROVEN | F_CNT, obstacle tasks (OB = true: dead cells count
+// nothing, landings on a cell masked at t+1 go to OUT in the epilogue, and
+// every realization from which some action's landing slot needs the exact
+// transit test -- danger class 2 / 3 -- takes the exact path for all its
+// rows).  Returns false when some cell cannot be binned or (lean) too many
+// realizations need the exact path; the caller then runs the per-transition
+// path (which clears its own histogram).  On success the task's dense
+// [slot][row] histogram at wbase + off_bdense holds exactly the counts the
+// per-transition path would produce.
+template <int FLAGS, bool OB>
 __device__ __forceinline__ bool bin_task(const BuildK *__restrict__ Kg, unsigned char *wbase, const BinEnt *tab_s, int t,
                                          int grp, int ag, const RowC &Rf, int outq, bool row_ok, int cs_row,
-                                         unsigned half_one)
+                                         unsigned half_one, const uint32_t *danger)
 {
     const BuildK &K = *Kg;
     const int lane = threadIdx.x & 31;
     const int CW = K.CW;
+    const int CWD = 2 * ((K.nslot + 31) >> 5);   // danger-map words per cell
+    // cells of the task that bin (obstacle tasks: dead cells -- the target,
+    // obstacle cells at t -- send every realization to OUT, model_builder.py:445-452)
+    auto cell_live = [&](int cs) {
+        const int lc = grp * CW + cs;
+        if (cs >= CW || lc >= K.ncell) return false;
+        if (OB) {
+            const int c = K.cell0 + lc;
+            if (c == K.tcell || K.mask[(size_t)t * K.nc + c]) return false;
+        }
+        return true;
+    };
+    if (OB && K.AG > 16) return false;   // the row masks take a bin's high half
     // every cell must fit before anything is written
     for (int p = 0; p < CW; p += 2) {
         int words = 0;
         for (int q = 0; q < 2; ++q) {
-            const int cs = p + q, lc = grp * CW + cs;
-            if (cs < CW && lc < K.ncell) {
+            if (cell_live(p + q)) {
                 BinCell B;
                 int w;
-                if (!bin_setup(K, t, K.cell0 + lc, B, w)) return false;
+                if (!bin_setup(K, t, K.cell0 + grp * CW + p + q, B, w)) return false;
                 words += w;
             }
         }
-        if (words > K.bin_words) return false;
+        if (words > K.bin_words - 32) return false;   // + 32 per-lane dummy counters (bin_loop)
     }
     uint32_t *bins = reinterpret_cast<uint32_t *>(wbase + K.off_bins);
     uint32_t *bq = reinterpret_cast<uint32_t *>(wbase + K.off_bq);
     const unsigned bins_s = (unsigned)__cvta_generic_to_shared(bins);
-    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(wbase + K.off_bdense);   // ring, then dense
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(wbase + K.off_bring);
     uint16_t *h16 = reinterpret_cast<uint16_t *>(wbase + K.off_bdense) + lane;
     uint16_t *h16q = h16 + Rf.soff * 32;
     const unsigned hs_word = (unsigned)__cvta_generic_to_shared(h16q) & ~3u;
     const int k1x = K.bin_k1x, k1y = K.bin_k1y;
     const int a = ag * 32 + (lane - cs_row * K.AG);
+    const uint32_t *cls_row = danger + cs_row * CWD;
+    const bool live_row = row_ok && (!OB || !(Rf.rflags & RF_DEAD));
+    const unsigned dense_s = (unsigned)__cvta_generic_to_shared(wbase + K.off_bdense);
+    ObstDrainBuf *db = reinterpret_cast<ObstDrainBuf *>(wbase + K.off_bq + kBinQO * 4);
+    uint8_t *mwin = reinterpret_cast<uint8_t *>(db + 1);   // [CW][2hy + 3][2hx + 3] mask at t
+    const double *ftab_s = reinterpret_cast<const double *>(tab_s + 2 * (K.bin_ns + 1) * kBinRep);
+    auto drain_all = [&](int qn) {
+#ifdef FM_STATS
+        const long long c0 = clock64();
+#endif
+        for (int n = qn; n > 0;) {
+            if (OB) n = bin_drain_obst<FLAGS>(K, bq, bins, n, t, grp, ag, dense_s, danger, CWD, db, ftab_s, mwin);
+            else n = bin_drain<FLAGS>(K, bq, n, t, grp, Rf, h16q, hs_word, outq, live_row, cs_row, half_one);
+        }
+#ifdef FM_STATS
+        if (OB && lane == 0)
+            g_fm_wcnt[(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % (148 * 64)][5] += (unsigned)((clock64() - c0) >> 6);
+#endif
+    };
+    if (OB) {   // the ring sits beside the dense histogram: zero it up front (mid-loop drains)
+        for (int sl = 0; sl <= K.nslot; ++sl) h16[sl * 32] = 0;
+        const int ww = 2 * K.hx + 3, wh = 2 * K.hy + 3;
+        if (lane < CW) {
+            const int c = K.cell0 + grp * CW + lane, ci = c % K.nx, cj = c / K.nx;
+            db->ci[lane] = ci;
+            db->cj[lane] = cj;
+            db->x0[lane] = make_double2(DADD(K.ox, DMUL(DADD((double)ci, 0.5), K.dx)),
+                                        DADD(K.oy, DMUL(DADD((double)cj, 0.5), K.dx)));
+            db->soff[lane] = -((cj - K.hy) * K.width + (ci - K.hx));
+        }
+        if (lane < min(K.AG, K.na - ag * 32)) {
+            const fm_action A = K.act[ag * 32 + lane];
+            db->act[lane] = make_double2(A.ax, A.ay);
+        }
+        for (int cs = 0; cs < CW; ++cs) {
+            if (!cell_live(cs)) continue;
+            const int c = K.cell0 + grp * CW + cs, i0 = c % K.nx - K.hx - 1, j0 = c / K.nx - K.hy - 1;
+            for (int k = lane; k < ww * wh; k += 32) {
+                const int i = i0 + k % ww, j = j0 + k / ww;
+                mwin[cs * ww * wh + k] =
+                    ((unsigned)i < (unsigned)K.nx && (unsigned)j < (unsigned)K.ny) ? K.mask[(size_t)t * K.nc + j * K.nx + i] : 0;
+            }
+        }
+        __syncwarp();
+    }
     for (int p = 0; p < CW; p += 2) {
+        // the pair's live cells, compacted (constant indices keep B in registers)
+        const bool l0 = cell_live(p), l1 = cell_live(p + 1);
+        const bool two = l0 && l1;
+        const int ncl = (l0 ? 1 : 0) + (l1 ? 1 : 0);
+        const int cid[2] = {l0 ? p : p + 1, p + 1};
         BinCell B[2];
-        bool has[2];
         int words = 0;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-            const int cs = p + q, lc = grp * CW + cs;
-            has[q] = cs < CW && lc < K.ncell;
             int w = 0;
-            if (has[q]) bin_setup(K, t, K.cell0 + lc, B[q], w);
+            if (q < ncl) {
+                bin_setup(K, t, K.cell0 + grp * CW + cid[q], B[q], w);
+            } else {   // a missing cell still runs through the loop: finite inputs (table indices)
+                B[q].bx = B[q].by = B[q].offx = B[q].offy = 0;
+                B[q].mu = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int m = 0; m < 8; ++m) B[q].md[m] = make_float2(0.f, 0.f);
+            }
             B[q].base = words;
             words += w;
-            if (!has[q]) B[q].bx = B[q].by = B[q].offx = B[q].offy = 0;
         }
-        for (int w = lane; w < words; w += 32) bins[w] = 0u;
+#ifdef FM_STATS
+        const long long ci0 = clock64();
+#endif
+        if (OB) {
+            // high half of each bin: the rows (task-local actions) whose
+            // landing from it lies on a slot of class 2 / 3 (the tight or
+            // grown box touches the mask at t: exact transit test)
+            const int na_loc = min(K.AG, K.na - ag * 32);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q >= ncl) continue;
+                const uint32_t *cl = danger + cid[q] * CWD;
+                bool anyg = false;
+                for (int i = 0; i < CWD; ++i) anyg |= (cl[i] & 0xAAAAAAAAu) != 0u;
+                uint32_t *b = bins + B[q].base;
+                const int bxn = B[q].bx, nw = B[q].bx * B[q].by;
+                for (int w = lane; w < nw; w += 32) {
+                    uint32_t g = 0u;
+                    if (anyg) {
+                        const int by = w / bxn, bx = w - by * bxn;
+                        const int bax = bx + B[q].offx, bay = by + B[q].offy;
+                        const int nxv = floordiv_pos(bax, k1x), sxv = bax - nxv * k1x;
+                        const int nyv = floordiv_pos(bay, k1y), syv = bay - nyv * k1y;
+                        for (int al = 0; al < na_loc; ++al) {
+                            const BinAct ba = K.bact[ag * 32 + al];
+                            const int di = ba.gx + nxv + (sxv >= ba.rx ? 1 : 0);
+                            const int dj = ba.gy + nyv + (syv >= ba.ry ? 1 : 0);
+                            if ((unsigned)(di + K.hx) <= (unsigned)(2 * K.hx) &&
+                                (unsigned)(dj + K.hy) <= (unsigned)(2 * K.hy)) {
+                                const int slot = (dj + K.hy) * K.width + di + K.hx;
+                                if ((cl[slot >> 4] >> ((slot & 15) << 1)) & 2u) g |= 1u << al;
+                            }
+                        }
+                    }
+                    b[w] = g << 16;
+                }
+            }
+        } else {
+            for (int w = lane; w < words; w += 32) bins[w] = 0u;
+        }
         __syncwarp();
-        const int qn = has[1] ? bin_loop<2>(K, B, p, t, tab_s, bins_s, ring_s, bq)
-                              : bin_loop<1>(K, B, p, t, tab_s, bins_s, ring_s, bq);
+#ifdef FM_STATS
+        const long long ci1 = clock64();
+        if (OB && lane == 0) g_fm_wcnt[(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % (148 * 64)][4] += (unsigned)((ci1 - ci0) >> 6);
+#endif
+        int qn = 0;
+        constexpr int RING = OB ? kBinRingO : kBinRing;
+        // one loop instance (code size): a missing second cell never counts
+        if (ncl > 0) qn = bin_loop<2, OB, RING>(K, B, cid, two, t, tab_s, bins_s, ring_s, bq, drain_all);
         if (qn < 0) return false;
         FM_STAT(5, lane == 0 ? 1 : 0);
-        // the ring is done: its space becomes the dense histogram (zeroed
-        // once, at the first pair), then the doubtful realizations go in
-        if (p == 0) {
+#ifdef FM_STATS
+        if (OB && lane == 0) g_fm_wcnt[(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % (148 * 64)][6] += (unsigned)((clock64() - ci1) >> 6);
+#endif
+        // lean tasks: the ring is done, its space becomes the dense histogram
+        // (zeroed once, at the first pair); then the deferred realizations
+        if (!OB && p == 0) {
             for (int sl = 0; sl <= K.nslot; ++sl) h16[sl * 32] = 0;
             __syncwarp();
         }
-        for (int n = qn; n > 0;) n = bin_drain<FLAGS>(K, bq, n, t, grp, Rf, h16q, hs_word, outq, row_ok, cs_row, half_one);
+        drain_all(qn);
         asm volatile("" ::: "memory");
         __syncwarp();
+        if (OB) {   // drop the row masks: the low halves are the counts
+            for (int w = lane; w < words; w += 32) bins[w] &= 0xFFFFu;
+            __syncwarp();
+        }
         // 2-D inclusive prefix sums of each cell's bins (rows, then columns)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -1829,9 +2222,9 @@ __device__ __forceinline__ bool bin_task(const BuildK *__restrict__ Kg, unsigned
         }
         __syncwarp();
         // each row: its (di, dj) counts are rectangle sums over the bins
-        if (row_ok && (cs_row == p || cs_row == p + 1)) {
+        if (live_row && ncl > 0 && (cs_row == cid[0] || (two && cs_row == cid[1]))) {
             // the row's cell (selects keep B in registers: no dynamic index)
-            const bool q1 = cs_row == p + 1;
+            const bool q1 = two && cs_row == cid[1];
             const int offx = q1 ? B[1].offx : B[0].offx, offy = q1 ? B[1].offy : B[0].offy;
             const int cbx = q1 ? B[1].bx : B[0].bx, cby = q1 ? B[1].by : B[0].by;
             const uint32_t *b = bins + (q1 ? B[1].base : B[0].base);
@@ -1856,10 +2249,22 @@ __device__ __forceinline__ bool bin_task(const BuildK *__restrict__ Kg, unsigned
                     if (x0 > 0 && y0 > 0) cnt += b[(y0 - 1) * cbx + x0 - 1];
                     if (cnt) {
                         // inside the window by the F_PROVEN proof
-                        if ((unsigned)(di + K.hx) <= (unsigned)(2 * K.hx) && (unsigned)(dj + K.hy) <= (unsigned)(2 * K.hy))
-                            h16q[((Rf.cj + dj) * K.width + (Rf.ci + di)) * 32] += (uint16_t)cnt;
-                        else
+                        if ((unsigned)(di + K.hx) <= (unsigned)(2 * K.hx) && (unsigned)(dj + K.hy) <= (unsigned)(2 * K.hy)) {
+                            int qq = (Rf.cj + dj) * K.width + (Rf.ci + di);
+                            if (OB) {
+                                // class 1: the landing cell is masked at t+1 -> OUT;
+                                // a 32-bit add (see bin_drain_obst)
+                                const int slot = qq + Rf.soff;
+                                if (((cls_row[slot >> 4] >> ((slot & 15) << 1)) & 3u) == 1u) qq = outq;
+                                asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(hs_word + (unsigned)qq * 64u),
+                                             "r"(half_one * cnt)
+                                             : "memory");
+                            } else {
+                                h16q[qq * 32] += (uint16_t)cnt;
+                            }
+                        } else {
                             atomicOr(K.viol + (size_t)t * K.na + a, 2u);   // cannot happen: flags a bug loudly
+                        }
                     }
                 }
             }
@@ -1895,21 +2300,33 @@ static_assert(FM_BUILD_RC <= 64, "chunk_rows_obst_cnt marks deferred realization
 #ifndef FM_BUILD_MINB1
 #define FM_BUILD_MINB1 3
 #endif
+// PART 3 / 4: lean / obstacle tasks by binning only (bin_task); a task that
+// cannot bin is appended to K.task_list and run by a PART 0 launch over the
+// list, so these launches carry no per-transition code (instruction cache).
 template <int FLAGS, int PART>
-__global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) ? FM_BUILD_MINB1
+__global__ void __launch_bounds__(128, (PART != 0 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) ? FM_BUILD_MINB1
                                                                                               : FM_BUILD_MINB)
     k_build(const __grid_constant__ BuildK K)
 {
+    constexpr bool OBST_PART = PART == 2 || PART == 4, LEAN_PART = PART == 1 || PART == 3, BINONLY = PART >= 3;
     const BuildK *__restrict__ Kg = &K;   // the parameter block, for the noinline rare paths
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *wbase = smem + K.off_block + (size_t)warp * K.smem_warp;
     // bin tables (lean tasks binned per realization): block-shared copy
     const BinEnt *tab_s = reinterpret_cast<const BinEnt *>(smem);
-    if constexpr (PART == 1 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) {
+    if constexpr (PART != 0 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) {
         if (K.bin_ok) {
-            BinEnt *t_s = reinterpret_cast<BinEnt *>(smem);
-            for (int i = threadIdx.x; i < 2 * (kBinNS + 1); i += blockDim.x) t_s[i] = K.tab[i];
+            BinEnt *t_s = reinterpret_cast<BinEnt *>(smem);   // [axis][bucket][kBinRep copies]
+            const int per_axis = (K.bin_ns + 1) * kBinRep;
+            for (int i = threadIdx.x; i < 2 * per_axis; i += blockDim.x) {
+                const int ax = i / per_axis, bkt = (i - ax * per_axis) / kBinRep;
+                t_s[i] = K.tab[ax * (kBinNS + 1) + bkt];
+            }
+            if (OBST_PART) {
+                double *f_s = reinterpret_cast<double *>(t_s + 2 * per_axis);
+                for (int i = threadIdx.x; i < (kFracSmemN + 1) * (kFracSmemN + 2) / 2; i += blockDim.x) f_s[i] = g_frac[i];
+            }
             __syncthreads();
         }
     }
@@ -1945,7 +2362,16 @@ __global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAG
         unsigned task = 0;
         if (lane == 0) task = atomicAdd(K.task_counter, 1u);
         task = __shfl_sync(kFull, task, 0);
-        if ((long long)task >= K.n_tasks) break;
+        if (PART == 0 && K.task_list) {   // the tasks the bin-only launches could not bin
+            if (task >= *K.task_list_n) break;
+            task = K.task_list[task];
+        } else if ((long long)task >= K.n_tasks) {
+            break;
+        }
+#ifdef FM_STATS
+        const long long tclk0 = clock64();
+        int tpath = 0;
+#endif
         h16 = hist16 + lane;
         const int per_t = K.groups * K.nag;
         const int t = K.t0 + (int)(task / per_t);
@@ -2011,7 +2437,7 @@ __global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAG
         if (PART != 0) {
             const bool obst_task =
                 !horizon && __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
-            if (obst_task != (PART == 2)) continue;   // the other launch's task
+            if (obst_task != OBST_PART) continue;   // the other launch's task
         }
 
         if (horizon) {
@@ -2029,8 +2455,8 @@ __global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAG
         } else {
             const bool edge = __any_sync(kFull, edge_row);
             const unsigned rowmask = __ballot_sync(kFull, row_ok);   // lanes that run chunk_rows
-            const bool obst = PART == 1   ? false
-                              : PART == 2 ? true
+            const bool obst = LEAN_PART   ? false
+                              : OBST_PART ? true
                                           : __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
             const int DW = (nslot + 31) >> 5, CWD = 2 * DW;   // class words per cell
             if (obst) {
@@ -2085,9 +2511,17 @@ __global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAG
             const int outq = nslot - R.soff;
             uint16_t *h16q = h16 + R.soff * 32;
             bool binned = false;
-            if constexpr (PART == 1 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) {
+            if constexpr (PART != 0 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) {
                 if (K.bin_ok) {
-                    binned = bin_task<FLAGS>(Kg, wbase, tab_s, t, grp, ag, Rf, outq, row_ok, cs_row, half_one);
+                    binned = bin_task<FLAGS, OBST_PART>(Kg, wbase, tab_s, t, grp, ag, Rf, outq, row_ok, cs_row,
+                                                        half_one, danger);
+#ifdef FM_STATS
+                    tpath = binned ? 1 : 2;
+#endif
+                    if (BINONLY && !binned) {   // to the list launch (per-transition code)
+                        if (lane == 0) K.task_list[atomicAdd(K.task_list_n, 1u)] = task;
+                        continue;
+                    }
                     if (binned) {
                         h16 = reinterpret_cast<uint16_t *>(wbase + K.off_bdense) + lane;
                     } else {
@@ -2098,7 +2532,7 @@ __global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAG
                     }
                 }
             }
-            if (!binned) {
+            if (!BINONLY && !binned) {
             // stage the CW cells' modes
             for (int i = lane; i < CW * nm; i += 32) {
                 const int cs = i / nm, m = i - (i / nm) * nm;
@@ -2295,6 +2729,20 @@ __global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAG
         }
 
         if (__any_sync(kFull, viol) && viol && row_ok) atomicOr(K.viol + (size_t)t * K.na + a, 1u);
+#ifdef FM_STATS
+        if (OBST_PART && lane == 0) {
+            const unsigned slot = atomicAdd(&g_fm_tcount, 1u);
+            const unsigned gw = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % (148 * 64);
+            if (slot < (1u << 17)) {
+                g_fm_ttimes[slot] = ((unsigned long long)task << 40) | ((unsigned long long)tpath << 36) |
+                                    (unsigned long long)min(clock64() - tclk0, (long long)((1ll << 36) - 1));
+                for (int k = 0; k < 8; ++k) {
+                    g_fm_ttimes[(1u << 18) + slot * 8 + k] = g_fm_wcnt[gw][k];
+                    g_fm_wcnt[gw][k] = 0;
+                }
+            }
+        }
+#endif
 
         // ---- emit: nnz census, warp scan, bump allocation, slot-ordered fill
         int nnz = 0;
@@ -2325,7 +2773,7 @@ __global__ void __launch_bounds__(128, (PART == 1 && (FLAGS & F_PROVEN) && (FLAG
             }
         }
         __syncwarp();
-        if (PART == 1 && h16 != hist16 + lane) {
+        if (PART != 0 && h16 != hist16 + lane) {
             // a binned task: its counters overlaid the per-transition
             // histogram, which every task expects zeroed
             uint4 *z = reinterpret_cast<uint4 *>(hist16);
@@ -2451,10 +2899,35 @@ static void bin_layout(BuildK &K)
     if (words < floor_words) words = floor_words;
     K.bin_words = words;
     K.off_bdense = align16(words * 4);
+    K.off_bring = K.off_bdense;
     K.off_bq = K.off_bdense + uni;
     const int end = align16(K.off_bq + q);
     if (end > K.smem_warp) K.smem_warp = end;
-    K.off_block = align16(2 * (kBinNS + 1) * (int)sizeof(BinEnt));
+    K.off_block = align16(2 * (K.bin_ns + 1) * kBinRep * (int)sizeof(BinEnt));
+}
+
+// Obstacle tasks (PART 2) by binning: bin counters | coefficient ring
+// (kBinRingO chunks) | dense histogram | queue (kBinQO), all live at once
+// (the queue drains mid-loop), then the danger map past both this and the
+// per-transition layout (a task that cannot bin falls back to the latter).
+// False when it does not fit a block's shared memory.
+static bool bin_layout_obst(BuildK &K)
+{
+    const int legacy_end = K.smem_warp;
+    const int words = K.CW >= 2 ? 1024 : 2048;
+    K.bin_words = words;
+    K.off_bins = 0;
+    K.off_bring = align16(words * 4);
+    K.off_bdense = align16(K.off_bring + kBinRingO * 32 * 32);
+    K.off_bq = align16(K.off_bdense + (K.nslot + 1) * 64);
+    const int end = align16(K.off_bq + kBinQO * 4 + (int)sizeof(ObstDrainBuf) +
+                            K.CW * (2 * K.hx + 3) * (2 * K.hy + 3));
+    K.off_danger = align16(end > legacy_end ? end : legacy_end);
+    K.smem_warp = align16(K.off_danger + 2 * K.CW * ((K.nslot + 31) / 32) * 4);
+    // bin tables, then fl(q / n) for n <= kFracSmemN
+    K.off_block = align16(2 * (K.bin_ns + 1) * kBinRep * (int)sizeof(BinEnt) +
+                          (kFracSmemN + 1) * (kFracSmemN + 2) / 2 * (int)sizeof(double));
+    return K.off_block + K.smem_warp <= smem_block_optin();
 }
 
 template <int FL, int PART>
@@ -2498,6 +2971,42 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
         return launch_build_p<FL, 0>(K, smem, s);
     } else {
         int32_t st;
+        if constexpr ((FL & F_CNT) != 0 && (FL & F_NET) == 0) {
+            if (K.bin_ok && !getenv("FM_NO_BINONLY")) {
+                // bin-only launches (lean, then obstacle tasks); the tasks
+                // they cannot bin run per transition in a PART 0 launch over
+                // the list they append to
+                unsigned int *list = nullptr;
+                FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&list), sizeof(unsigned int) * ((size_t)K.n_tasks + 1), s));
+                FM_CK(cudaMemsetAsync(list + K.n_tasks, 0, sizeof(unsigned int), s));
+                BuildK K1 = K;
+                K1.task_list = list;
+                K1.task_list_n = list + K.n_tasks;
+                st = launch_build_p<FL, 3>(K1, smem, s);
+                if (st == FM_OK) {
+                    BuildK K2 = K1;
+                    K2.off_block = 0;
+                    smem_layout_fit(K2, kQueue, false);
+                    if (!getenv("FM_NO_OBST_BINS") && bin_layout_obst(K2)) {
+                        st = launch_build_p<FL, 4>(K2, (size_t)4 * K2.smem_warp, s);
+                    } else {
+                        K2.bin_ok = 0;
+                        K2.off_block = 0;
+                        smem_layout_fit(K2, kQueue, false);
+                        st = launch_build_p<FL, 2>(K2, (size_t)4 * K2.smem_warp, s);
+                    }
+                }
+                if (st == FM_OK) {
+                    BuildK K0 = K1;
+                    K0.bin_ok = 0;
+                    K0.off_block = 0;
+                    smem_layout_fit(K0, kQueue, false);
+                    st = launch_build_p<FL, 0>(K0, (size_t)4 * K0.smem_warp, s);
+                }
+                FM_CK(cudaFreeAsync(list, s));
+                return st;
+            }
+        }
         if constexpr ((FL & F_NET) != 0) {
             // lean net-energy rows read h_cr * g[t+1] from a per-warp slot
             // table (half-size chunks keep 4 blocks per SM)
@@ -2515,6 +3024,11 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
             BuildK K2 = K;
             K2.off_block = 0;
             smem_layout_fit(K2, kQueue, false);
+            if (K2.bin_ok && (getenv("FM_NO_OBST_BINS") || !bin_layout_obst(K2))) {
+                K2.bin_ok = 0;
+                K2.off_block = 0;
+                smem_layout_fit(K2, kQueue, false);
+            }
             return launch_build_p<FL, 2>(K2, (size_t)4 * K2.smem_warp, s);
         } else {
             BuildK K2 = K;
@@ -2703,9 +3217,10 @@ static bool rewards_sum_exactly(const fm_build_args *h)
 // zone [min - dzone, max + dzone] routes realizations to the exact path, so
 // every realization outside all zones lies on one side of every step of the
 // cluster; steps near 0 or 1 join the unit boundary (always / never).
-static bool bin_axis(const std::vector<double> &comp, double p, double dz, int &k1, BinEnt *tab, int *g, int *r)
+static bool bin_axis(const std::vector<double> &comp, double p, double dz, int NS, int &k1, BinEnt *tab, int *g,
+                     int *r)
 {
-    const double eta = 1.0 / (8.0 * kBinNS), gap = 1.0 / kBinNS + 2.0 * eta;
+    const double eta = 1.0 / (8.0 * NS), gap = 1.0 / NS + 2.0 * eta;
     double hi0 = dz, lotop = 1.0 - dz;
     std::vector<int> bottom, top;
     std::vector<std::pair<double, int>> th;
@@ -2768,8 +3283,8 @@ static bool bin_axis(const std::vector<double> &comp, double p, double dz, int &
         memcpy(&r, &b, 4);
         return r;
     };
-    for (int b = 0; b <= kBinNS; ++b) {   // entry NS: frac == 1
-        const double elo = (double)b / kBinNS - eta, ehi = (double)(b + 1) / kBinNS + eta;
+    for (int b = 0; b <= NS; ++b) {   // entry NS: frac == 1
+        const double elo = (double)b / NS - eta, ehi = (double)(b + 1) / NS + eta;
         int kb = 0;
         for (int k = 0; k < K; ++k) kb += chi[k] < elo ? 1 : 0;
         float lo = 3.0f, hi = 3.0f;
@@ -2814,8 +3329,24 @@ static void bin_params(const fm_build_args *h, BuildK &K)
     const double kRel = (2.0 * K.nm + 8.0) * 0x1p-24 * 1.001;
     K.bin_dzone = fmax(0x1p-17, 2.0 * (T * kRel * ip + 0x1p-21 * (T * ip + 1.0) + K.bin_eps));
     std::vector<int> gx(K.na), rx(K.na), gy(K.na), ry(K.na);
-    if (!bin_axis(ax, p, K.bin_dzone, K.bin_k1x, K.tab, gx.data(), rx.data())) return;
-    if (!bin_axis(ay, p, K.bin_dzone, K.bin_k1y, K.tab + kBinNS + 1, gy.data(), ry.data())) return;
+    if (!bin_axis(ax, p, K.bin_dzone, kBinNS, K.bin_k1x, K.tab, gx.data(), rx.data())) return;
+    if (!bin_axis(ay, p, K.bin_dzone, kBinNS, K.bin_k1y, K.tab + kBinNS + 1, gy.data(), ry.data())) return;
+    K.bin_ns = kBinNS;
+    // coarser buckets shrink the replicated block-shared tables; accepted
+    // only when they give the same step clusters (hence the same zones)
+    for (int ns : {32, 64}) {
+        BinEnt tab[2 * (kBinNS + 1)];
+        int k1x = 0, k1y = 0;
+        if (bin_axis(ax, p, K.bin_dzone, ns, k1x, tab, gx.data(), rx.data()) &&
+            bin_axis(ay, p, K.bin_dzone, ns, k1y, tab + kBinNS + 1, gy.data(), ry.data()) && k1x == K.bin_k1x &&
+            k1y == K.bin_k1y) {
+            memcpy(K.tab, tab, sizeof(tab));
+            K.bin_ns = ns;
+            break;
+        }
+        bin_axis(ax, p, K.bin_dzone, kBinNS, k1x, K.tab, gx.data(), rx.data());   // restore
+        bin_axis(ay, p, K.bin_dzone, kBinNS, k1y, K.tab + kBinNS + 1, gy.data(), ry.data());
+    }
     for (int a = 0; a < K.na; ++a) K.bact[a] = BinAct{gx[a], rx[a], gy[a], ry[a]};
     K.bin_p = p;
     K.bin_p1 = p == 1.0 ? 1 : 0;
@@ -2823,6 +3354,9 @@ static void bin_params(const fm_build_args *h, BuildK &K)
     K.envelope = reinterpret_cast<const int4 *>(h->envelope);
     K.bin_ok = 1;
     bin_layout(K);
+    if (getenv("FM_BIN_DEBUG"))
+        fprintf(stderr, "bin: ns %d k1 (%d, %d) dzone %.3g words %d smem_warp %d off_block %d\n", K.bin_ns, K.bin_k1x,
+                K.bin_k1y, K.bin_dzone, K.bin_words, K.smem_warp, K.off_block);
 }
 
 // validates the arguments and fills the kernel parameter block + flags
@@ -2854,6 +3388,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.dx = G.dx; K.dt = G.dt; K.ox = G.ox; K.oy = G.oy;
     K.inv_dx = 1.0 / G.dx;
     K.half_dx = 0.5 * G.dx;   // `0.5 * grid.dx` (environment.py:356)
+    K.inv_half_dx = 1.0 / K.half_dx;   // exact for a power-of-two dx (the only case it is used)
     K.mean = h->env.mean; K.modes = h->env.modes; K.coeffs = h->env.coeffs; K.g = h->env.g;
     K.mask = h->env.mask; K.sat = h->mask_sat;
     K.nm = h->env.n_modes; K.nr = h->env.n_real;
@@ -2930,18 +3465,18 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
 
 // Bin path inputs for slabs [t0, t1): f32 coefficients padded to 8 modes
 // ([t - t0][r][8]) and max_r |coeff| per (t, m) (the error bound's T).
-__global__ void k_bin_prep(const double *coeffs, int t0, int nts, int nr, int nm, float *c32, double *cmax)
+__global__ void k_bin_prep(const double *coeffs, int t0, int nts, int nr, int nr_pad, int nm, float *c32, double *cmax)
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (long long)nts * nr) return;
-    const int tl = (int)(i / nr);
-    const double *src = coeffs + ((size_t)(t0 + tl) * nr + (i % nr)) * nm;
+    if (i >= (long long)nts * nr_pad) return;
+    const int tl = (int)(i / nr_pad), r = (int)(i % nr_pad);
+    const double *src = coeffs + ((size_t)(t0 + tl) * nr + r) * nm;
     float out[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-        const double c = m < nm ? src[m] : 0.0;
+        const double c = (m < nm && r < nr) ? src[m] : 0.0;
         out[m] = (float)c;
-        if (m < nm)
+        if (m < nm && r < nr)
             atomicMax(reinterpret_cast<unsigned long long *>(cmax + (size_t)tl * nm + m),
                       (unsigned long long)__double_as_longlong(fabs(c)));   // non-negative: bits order
     }
@@ -2964,11 +3499,12 @@ extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *st
     double *cmax = nullptr;
     if (K.bin_ok) {
         const int nts = K.t1 - K.t0;
-        FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&c32), sizeof(float) * 8 * (size_t)nts * K.nr, s));
+        K.nr_pad = (K.nr + 127) & ~127;   // whole iterations of up to 4 chunks
+        FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&c32), sizeof(float) * 8 * (size_t)nts * K.nr_pad, s));
         FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&cmax), sizeof(double) * (size_t)nts * (K.nm ? K.nm : 1), s));
         FM_CK(cudaMemsetAsync(cmax, 0, sizeof(double) * (size_t)nts * (K.nm ? K.nm : 1), s));
-        const long long n = (long long)nts * K.nr;
-        k_bin_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(K.coeffs, K.t0, nts, K.nr, K.nm, c32, cmax);
+        const long long n = (long long)nts * K.nr_pad;
+        k_bin_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(K.coeffs, K.t0, nts, K.nr, K.nr_pad, K.nm, c32, cmax);
         FM_CK_LAUNCH("k_bin_prep");
         K.coef32 = c32;
         K.cmax = cmax;

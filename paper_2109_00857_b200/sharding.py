@@ -282,9 +282,12 @@ class StripPlanner:
         if pipelined:
             main.wait_stream(ss)
 
-    def step(self, scanned: bool = False):
+    def step(self, scanned: bool = False, sink: dict | None = None, sink_stream=None):
         """One planner step; returns the strip's DeviceModel (values /
-        policy in ``self.values`` / ``self.policy``)."""
+        policy in ``self.values`` / ``self.policy``).  With ``sink`` (pinned
+        host buffers, DeviceModel.host_buffers) the compact model streams to
+        the host on ``sink_stream`` group by group while the build runs;
+        ``self.sink_bytes`` = the bytes copied."""
         import torch
 
         from .builder import build_device_model, subgrid_from_vmax
@@ -292,9 +295,10 @@ class StripPlanner:
         if not scanned:
             de.reset_derived()
         ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-        self.events = {"start": ev(), "built": ev(), "solved": ev()}
+        self.events = {"start": ev(), "scanned": ev(), "built": ev(), "solved": ev()}
         self.events["start"].record()
         vm = de.velocity_max(j_range=(self.j0, self.j1), group=self.group) if self.world > 1 else de.velocity_max()
+        self.events["scanned"].record()
         sub = subgrid_from_vmax(vm, self.actions.f_max, g, self.buffer)
         dm = build_device_model(de, self.actions, self.rcfg, self.target, sub, j_range=(self.j0, self.j1),
                                 defer_check=True, reuse=self.dm, t_groups=slab_groups(g.nt, self.n_groups),
@@ -303,7 +307,12 @@ class StripPlanner:
         self.events["built"].record()
         self._solve(dm, pipelined=True)
         self.events["solved"].record()
-        self._finish(dm)
+        self.sink_bytes = 0
+        if sink is not None:
+            self.sink_bytes = dm.stream_to_host(sink, sink_stream)
+        if self._finish(dm) and sink is not None:   # rebuilt (capacity): copy the final model again
+            sink_stream.wait_stream(torch.cuda.current_stream())
+            self.sink_bytes = dm.copy_to_host(sink, sink_stream)
         return dm
 
     def _finish(self, dm):
@@ -326,3 +335,4 @@ class StripPlanner:
             raise err
         if rebuilt:   # capacity miss somewhere: the model was rebuilt, solve again (all ranks)
             self._solve(dm, pipelined=False)
+        return rebuilt

@@ -419,17 +419,20 @@ def test_scanned_upload_matches_full_scan(slabs):
         assert torch.equal(dp.modes, ref.modes) and dp.velocity_max() == full
 
 
-@pytest.mark.parametrize("case", ["desk", "paper_1k", "zero_flow", "random"])
+@pytest.mark.parametrize("case", ["desk", "paper_1k", "two_obstacles_1k", "zero_flow", "random"])
 def test_binned_build_equals_per_transition_build(case, monkeypatch):
-    """Lean cells binned per (cell, realization) (k_build's bin path, with
-    the scan's per-cell envelope or the in-kernel triangle bound) give the
-    same model as the per-transition path (FM_NO_BINS), entry for entry."""
+    """Cells binned per (cell, realization) (k_build's bin path, with the
+    scan's per-cell envelope or the in-kernel triangle bound; lean tasks and
+    obstacle tasks) give the same model as the per-transition path
+    (FM_NO_BINS) and as binning lean tasks only (FM_NO_OBST_BINS), entry for
+    entry."""
     import torch
     if case == "desk":
         env, acts, rcfg, target, _ = make_named_env("desk")
-    elif case == "paper_1k":
+    elif case in ("paper_1k", "two_obstacles_1k"):
         from paper_2109_00857_b200 import workloads
-        w = workloads.get("paper").with_(n_realizations=1000)
+        w = workloads.get("paper" if case == "paper_1k" else "paper_net_energy").with_(
+            n_realizations=1000, objective="time")
         env, acts, rcfg, target = w.environment(), w.actions(), w.reward_config(), w.target
     elif case == "zero_flow":   # every realization sits exactly on a step: all take the exact path
         env = make_zero_flow_env(nx=12, ny=12, nt=5, n_realizations=64)
@@ -448,7 +451,9 @@ def test_binned_build_equals_per_transition_build(case, monkeypatch):
     denv._env_rows = None                     # no envelope: triangle bound around the mean
     tri = flat(build_device_model(denv, acts, rcfg, target, sub))
     denv._env_rows = saved
+    monkeypatch.setenv("FM_NO_OBST_BINS", "1")
+    lean_only = flat(build_device_model(denv, acts, rcfg, target, sub))
     monkeypatch.setenv("FM_NO_BINS", "1")
     ref = flat(build_device_model(denv, acts, rcfg, target, sub))
-    assert binned == ref and tri == ref
+    assert binned == ref and tri == ref and lean_only == ref
     torch.cuda.synchronize()
