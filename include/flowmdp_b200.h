@@ -141,6 +141,15 @@ typedef struct {
      * exchange's communication kernels) run while the build proceeds.  0 =
      * the whole GPU. */
     int32_t reserve_sms;
+    /* Which tasks of [t0, t1) x [j0, j1) this call builds: bit 0 = lean
+     * tasks (no obstacle or dead cell near any row of the task), bit 1 =
+     * obstacle tasks; 0 = all (same as 3).  A pipelined caller builds the
+     * obstacle tasks of the whole range first and then the lean tasks slab
+     * group by slab group, so each group completes with one short launch
+     * (its rows, and the entries it appends, are final when that launch
+     * ends).  Builds whose tasks cannot be told apart (no proven fast path)
+     * do everything in the lean phase. */
+    int32_t phases;
 } fm_build_args;
 
 /* Sub-grid overflow report (message of model_builder.py:433-438). */

@@ -664,9 +664,17 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
         if snap is None or snap.numel() < len(t_groups):
             snap = torch.zeros(len(t_groups), dtype=torch.int64).pin_memory()
         dm.group_nnz = snap
+        # the obstacle tasks of the whole range first (the slow ones), then
+        # the lean tasks group by group: each group completes with one short
+        # launch (fm_build_args.phases); its entries follow the obstacle
+        # launch's in the bump allocation
+        oa = _lib.FmBuildArgs.from_buffer_copy(args)
+        oa.phases = 2
+        _lib.check(L.fm_build_launch(C.byref(oa), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
         for k, (g0, g1) in enumerate(t_groups):
             ga = _lib.FmBuildArgs.from_buffer_copy(args)
             ga.t0, ga.t1 = int(g0), int(g1)
+            ga.phases = 1
             _lib.check(L.fm_build_launch(C.byref(ga), C.byref(m), _lib.stream_ptr()), "fm_build_launch")
             snap[k:k + 1].copy_(d_nnz, non_blocking=True)
             ev = torch.cuda.Event()

@@ -728,9 +728,14 @@ struct BuildK {
     uint32_t *viol;
     unsigned int *task_counter;
     unsigned int *task_list, *task_list_n;   // tasks the bin-only launches could not bin (PART 0 list launch)
+    // PART 3 / 4: the tasks of the launch from k_classify's lists: list a,
+    // then list b (PART 4: obstacle tasks near the obstacle first -- the
+    // longest ones -- then the rest)
+    const unsigned int *src_a, *src_b, *src_a_n, *src_b_n;
     uint16_t *ghist;   // F_GHIST: [resident warp][nslot + 1][32]
     // ---- per-(cell, realization) binning of lean tasks (see bin_task) ----
     int bin_ok;                 // the launch has bin tables (PART 1 lean tasks use them)
+    int dev_flags;              // development A/B switches (FM_DEV_FLAGS; 0 in production)
     int bin_k1x, bin_k1y;       // sub-bins per unit of z = v / p, per axis (clusters + 1)
     int bin_p1;                 // p = dx / dt == 1 (z = v)
     float bin_ip;               // f32(1 / p)
@@ -1812,7 +1817,7 @@ __device__ __noinline__ int bin_drain_obst(const BuildK &K, const uint32_t *bq, 
         atomicAdd(&g_fm_wcnt[gw][2], 1u);
         if (cl >= 2) atomicAdd(&g_fm_wcnt[gw][3], 1u);
 #endif
-        const bool blocked = cl >= 2 && seg_samples_blocked_win<FLAGS>(K, ftab_s, mwin + cs * ww * wh,
+        const bool blocked = cl >= 2 && !(K.dev_flags & 1) && seg_samples_blocked_win<FLAGS>(K, ftab_s, mwin + cs * ww * wh,
                                                                       R.ci - K.hx - 1, R.cj - K.hy - 1, ww, wh, t,
                                                                       R.x0, R.y0, x1, y1);
         const unsigned sh = (unsigned)(owner & 1) * 16u;
@@ -2365,6 +2370,15 @@ __global__ void __launch_bounds__(128, (PART != 0 && (FLAGS & F_PROVEN) && (FLAG
         if (PART == 0 && K.task_list) {   // the tasks the bin-only launches could not bin
             if (task >= *K.task_list_n) break;
             task = K.task_list[task];
+        } else if (BINONLY) {   // this launch's classified tasks
+            const unsigned na_ = *K.src_a_n;
+            if (task < na_) {
+                task = K.src_a[task];
+            } else {
+                task -= na_;
+                if (!K.src_b || task >= *K.src_b_n) break;
+                task = K.src_b[task];
+            }
         } else if ((long long)task >= K.n_tasks) {
             break;
         }
@@ -2437,7 +2451,12 @@ __global__ void __launch_bounds__(128, (PART != 0 && (FLAGS & F_PROVEN) && (FLAG
         if (PART != 0) {
             const bool obst_task =
                 !horizon && __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
-            if (obst_task != OBST_PART) continue;   // the other launch's task
+            if (obst_task != OBST_PART) {   // the other launch's task
+                // (bin-only launches get classified lists: a disagreement
+                // would be a bug -- the list launch still builds the task)
+                if (BINONLY && lane == 0) K.task_list[atomicAdd(K.task_list_n, 1u)] = task;
+                continue;
+            }
         }
 
         if (horizon) {
@@ -2520,6 +2539,11 @@ __global__ void __launch_bounds__(128, (PART != 0 && (FLAGS & F_PROVEN) && (FLAG
 #endif
                     if (BINONLY && !binned) {   // to the list launch (per-transition code)
                         if (lane == 0) K.task_list[atomicAdd(K.task_list_n, 1u)] = task;
+                        // the bin regions overlay the per-transition histogram,
+                        // which the next task (a horizon task) expects zeroed
+                        uint4 *z = reinterpret_cast<uint4 *>(hist16);
+                        for (int i = lane; i < (nslot + 1) * 4; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+                        __syncwarp();
                         continue;
                     }
                     if (binned) {
@@ -2930,6 +2954,51 @@ static bool bin_layout_obst(BuildK &K)
     return K.off_block + K.smem_warp <= smem_block_optin();
 }
 
+// warp-aggregated append of val to list (when pred)
+__device__ __forceinline__ void list_append(unsigned int *list, unsigned int *n, bool pred, unsigned int val)
+{
+    const unsigned act = __activemask(), m = __ballot_sync(act, pred);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(n, (unsigned)__popc(m));
+    base = __shfl_sync(act, base, leader);
+    if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = val;
+}
+
+// Task classes for the bin-only launches, with k_build's own test (a task is
+// an obstacle task when a row of it is dead or has the mask near its window,
+// model_builder.py:218-228, 247-259, 336-345): lean tasks (and the horizon)
+// -> list 0; obstacle tasks with the mask within two cells of a source cell
+// at t or t+1 (the slow ones: many exact transit tests) -> list 1; the
+// other obstacle tasks -> list 2.  lists = 3 arrays of n_tasks, n = 3 counters.
+__global__ void k_classify(const __grid_constant__ BuildK K, unsigned int *lists, unsigned int *n)
+{
+    const long long task = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (task >= K.n_tasks) return;
+    const int per_t = K.groups * K.nag;
+    const int t = K.t0 + (int)(task / per_t);
+    const int grp = (int)(task % per_t) / K.nag;
+    const int rx = K.gate_r ? __ldg(K.gate_r) : K.rx, ry = K.gate_r ? __ldg(K.gate_r + 1) : K.ry;
+    bool obst = false, near = false;
+    if (t + 1 < K.nt) {
+        for (int cs = 0; cs < K.CW; ++cs) {
+            const int lc = grp * K.CW + cs;
+            if (lc >= K.ncell) break;
+            const int c = K.cell0 + lc, ci = c % K.nx, cj = c / K.nx;
+            const bool dead = c == K.tcell || K.mask[(size_t)t * K.nc + c];
+            const bool segwin = box_count(K, t, ci - rx, ci + rx, cj - ry, cj + ry) > 0 &&
+                                box_count(K, t, ci - K.hx - 1, ci + K.hx + 1, cj - K.hy - 1, cj + K.hy + 1) > 0;
+            const bool landwin = box_count(K, t + 1, ci - K.hx, ci + K.hx, cj - K.hy, cj + K.hy) > 0;
+            obst |= dead || segwin || landwin;
+            near |= box_count(K, t, ci - 2, ci + 2, cj - 2, cj + 2) > 0 ||
+                    box_count(K, t + 1, ci - 2, ci + 2, cj - 2, cj + 2) > 0;
+        }
+    }
+    const int cls = !obst ? 0 : near ? 1 : 2;
+    for (int k = 0; k < 3; ++k) list_append(lists + (size_t)k * K.n_tasks, n + k, cls == k, (unsigned)task);
+}
+
 template <int FL, int PART>
 static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
 {
@@ -2965,26 +3034,39 @@ static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
 }
 
 template <int FL>
-static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
+static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s, int phases)
 {
     if constexpr (!(FL & F_PROVEN)) {
-        return launch_build_p<FL, 0>(K, smem, s);
+        return (phases & 1) ? launch_build_p<FL, 0>(K, smem, s) : FM_OK;   // one class: the lean phase
     } else {
-        int32_t st;
+        int32_t st = FM_OK;
         if constexpr ((FL & F_CNT) != 0 && (FL & F_NET) == 0) {
             if (K.bin_ok && !getenv("FM_NO_BINONLY")) {
                 // bin-only launches (lean, then obstacle tasks); the tasks
                 // they cannot bin run per transition in a PART 0 launch over
                 // the list they append to
+                // lists: [lean | near-obstacle | other obstacle | failed] x n_tasks, then 4 counters
                 unsigned int *list = nullptr;
-                FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&list), sizeof(unsigned int) * ((size_t)K.n_tasks + 1), s));
-                FM_CK(cudaMemsetAsync(list + K.n_tasks, 0, sizeof(unsigned int), s));
+                const size_t nt4 = 4 * (size_t)K.n_tasks;
+                FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&list), sizeof(unsigned int) * (nt4 + 4), s));
+                FM_CK(cudaMemsetAsync(list + nt4, 0, 4 * sizeof(unsigned int), s));
+                unsigned int *cnt = list + nt4;
+                k_classify<<<(unsigned)((K.n_tasks + 255) / 256), 256, 0, s>>>(K, list, cnt);
+                FM_CK_LAUNCH("k_classify");
                 BuildK K1 = K;
-                K1.task_list = list;
-                K1.task_list_n = list + K.n_tasks;
-                st = launch_build_p<FL, 3>(K1, smem, s);
-                if (st == FM_OK) {
+                K1.task_list = list + 3 * (size_t)K.n_tasks;
+                K1.task_list_n = cnt + 3;
+                K1.src_a = list;
+                K1.src_a_n = cnt;
+                K1.src_b = nullptr;
+                K1.src_b_n = cnt + 3;   // unused with src_b null
+                if (phases & 1) st = launch_build_p<FL, 3>(K1, smem, s);
+                if (st == FM_OK && (phases & 2)) {
                     BuildK K2 = K1;
+                    K2.src_a = list + (size_t)K.n_tasks;
+                    K2.src_a_n = cnt + 1;
+                    K2.src_b = list + 2 * (size_t)K.n_tasks;
+                    K2.src_b_n = cnt + 2;
                     K2.off_block = 0;
                     smem_layout_fit(K2, kQueue, false);
                     if (!getenv("FM_NO_OBST_BINS") && bin_layout_obst(K2)) {
@@ -3007,17 +3089,19 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s)
                 return st;
             }
         }
-        if constexpr ((FL & F_NET) != 0) {
-            // lean net-energy rows read h_cr * g[t+1] from a per-warp slot
-            // table (half-size chunks keep 4 blocks per SM)
-            BuildK K1 = K;
-            K1.off_block = 0;
-            smem_layout_fit(K1, 0, true);
-            st = launch_build_p<FL, 1>(K1, (size_t)4 * K1.smem_warp, s);
-        } else {
-            st = launch_build_p<FL, 1>(K, smem, s);
+        if (phases & 1) {
+            if constexpr ((FL & F_NET) != 0) {
+                // lean net-energy rows read h_cr * g[t+1] from a per-warp slot
+                // table (half-size chunks keep 4 blocks per SM)
+                BuildK K1 = K;
+                K1.off_block = 0;
+                smem_layout_fit(K1, 0, true);
+                st = launch_build_p<FL, 1>(K1, (size_t)4 * K1.smem_warp, s);
+            } else {
+                st = launch_build_p<FL, 1>(K, smem, s);
+            }
         }
-        if (st != FM_OK) return st;
+        if (st != FM_OK || !(phases & 2)) return st;
         if constexpr ((FL & F_CNT) != 0) {
             // obstacle part: per-warp queue of deferred exact segment tests
             // (half-size reconstruction chunks keep it at 4 blocks per SM)
@@ -3071,9 +3155,10 @@ static int32_t launch_build_ghist(BuildK K, cudaStream_t s)
     return FM_OK;
 }
 
-static int32_t launch_build(const BuildK &K, int flags, size_t smem, cudaStream_t s)
+static int32_t launch_build(const BuildK &K, int flags, size_t smem, cudaStream_t s, int phases)
 {
     if (flags & F_GHIST) {
+        if (!(phases & 1)) return FM_OK;   // one class: the lean phase
         // identity geometry flags dropped: x*1, x/1, x-0 are exact
         if (flags & F_NET) return launch_build_ghist<F_GHIST | F_NET>(K, s);
         return launch_build_ghist<F_GHIST>(K, s);
@@ -3085,7 +3170,7 @@ static int32_t launch_build(const BuildK &K, int flags, size_t smem, cudaStream_
         const int geo = (flags & 15) == (F_DT_ONE | F_OX_ZERO | F_DX_ONE) ? (flags & 15) : 0;
         switch (geo | (flags & (F_NET | F_PROVEN | F_CNT))) {
 #define FM_CASE(F) \
-    case F: return launch_build_t<F>(K, smem, s);
+    case F: return launch_build_t<F>(K, smem, s, phases);
             FM_CASE(11 | F_PROVEN) FM_CASE(11 | F_PROVEN | F_CNT) FM_CASE(11 | F_PROVEN | F_NET)
             FM_CASE(F_PROVEN) FM_CASE(F_PROVEN | F_CNT) FM_CASE(F_PROVEN | F_NET)
 #undef FM_CASE
@@ -3094,7 +3179,7 @@ static int32_t launch_build(const BuildK &K, int flags, size_t smem, cudaStream_
     }
     switch (flags) {
 #define FM_CASE(F) \
-    case F: return launch_build_t<F>(K, smem, s);
+    case F: return launch_build_t<F>(K, smem, s, phases);
         FM_CASE(0) FM_CASE(1) FM_CASE(2) FM_CASE(3) FM_CASE(4) FM_CASE(5) FM_CASE(6) FM_CASE(7)
         FM_CASE(8) FM_CASE(9) FM_CASE(10) FM_CASE(11) FM_CASE(16) FM_CASE(17) FM_CASE(18) FM_CASE(19)
         FM_CASE(20) FM_CASE(21) FM_CASE(22) FM_CASE(23) FM_CASE(24) FM_CASE(25) FM_CASE(26) FM_CASE(27)
@@ -3389,6 +3474,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
     K.inv_dx = 1.0 / G.dx;
     K.half_dx = 0.5 * G.dx;   // `0.5 * grid.dx` (environment.py:356)
     K.inv_half_dx = 1.0 / K.half_dx;   // exact for a power-of-two dx (the only case it is used)
+    K.dev_flags = getenv("FM_DEV_FLAGS") ? atoi(getenv("FM_DEV_FLAGS")) : 0;
     K.mean = h->env.mean; K.modes = h->env.modes; K.coeffs = h->env.coeffs; K.g = h->env.g;
     K.mask = h->env.mask; K.sat = h->mask_sat;
     K.nm = h->env.n_modes; K.nr = h->env.n_real;
@@ -3509,7 +3595,7 @@ extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *st
         K.coef32 = c32;
         K.cmax = cmax;
     }
-    st = launch_build(K, flags, (size_t)4 * K.smem_warp, s);
+    st = launch_build(K, flags, (size_t)4 * K.smem_warp, s, (h->phases & 3) ? (h->phases & 3) : 3);
     if (c32) FM_CK(cudaFreeAsync(c32, s));
     if (cmax) FM_CK(cudaFreeAsync(cmax, s));
     return st;

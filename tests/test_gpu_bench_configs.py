@@ -134,6 +134,45 @@ def test_bench_config_full_realizations(name):
     torch.cuda.empty_cache()
 
 
+def row_hashes(dm):
+    """Per-row digest of the entries (placement-independent: entries of a
+    row are in canonical slot order, hashed with their position)."""
+    import torch
+    cnt = dm.row_nnz.to(torch.int64) & 0xFFFF
+    seg = torch.repeat_interleave(torch.arange(cnt.numel(), device=cnt.device), cnt)
+    pos = torch.arange(int(cnt.sum()), device=cnt.device) - torch.repeat_interleave(torch.cumsum(cnt, 0) - cnt, cnt)
+    idx = torch.repeat_interleave(dm.row_ptr, cnt) + pos
+    ent = dm.entries[idx].to(torch.int64) & 0xFFFFFFFF
+    key = (ent * 1000003 + pos) * 2654435761 % 4294967291
+    return torch.zeros(cnt.numel(), dtype=torch.int64, device=cnt.device).index_add_(0, seg, key)
+
+
+@pytest.mark.parametrize("name", ["paper", "paper_net_energy"])
+def test_build_deterministic_full_realizations(name):
+    """Repeated builds of the benchmarked model give the same rows, rewards
+    and entries (only the entries' placement may differ): catches scratch
+    state leaking between the tasks of a persistent launch (every slab,
+    every row -- the oracle comparisons sample four slabs)."""
+    import torch
+    w = workloads.get(name)
+    env = w.environment()
+    acts, rcfg, target, g = w.actions(), w.reward_config(), w.target, w.grid
+    denv = DeviceEnv.from_host(env)
+    sub = subgrid_from_vmax(denv.velocity_max(), acts.f_max, g, w.buffer)
+    ref = None
+    for _ in range(3):
+        dm = build_device_model(denv, acts, rcfg, target, sub)
+        dm.check()
+        got = (dm.nnz, dm.row_nnz.clone(), dm.reward.clone(), row_hashes(dm))
+        if ref is None:
+            ref = got
+        else:
+            assert got[0] == ref[0]
+            assert torch.equal(got[1], ref[1]) and torch.equal(got[2], ref[2]) and torch.equal(got[3], ref[3])
+        del dm
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.slow
 def test_stress_c5_spot_checks():
     """C5 (400x400x200, 32 actions, 10,000 realizations; 1.02e13
