@@ -187,6 +187,17 @@ int32_t fm_velocity_max_slab(fm_grid grid, fm_env env, int32_t t0, int32_t t1, i
 int32_t fm_velocity_scan(fm_grid grid, fm_env env, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
                          double *d_out2, int32_t *d_envelope, void *stream);
 
+/* The same scan without the exact f64 recompute: d_out4 = (lo_x, hi_x,
+ * lo_y, hi_y), each combined by atomic max into the caller's (zeroed)
+ * buffer, with lo_c <= max |v_c| <= hi_c (the f32 envelope widened by the
+ * per-cell rounding bound; hi = +inf when an input is not finite), plus the
+ * envelope as above.  compute_subgrid (model_builder.py:376-399) needs only
+ * ceil((max|v_c| + f_max) dt / dx): when lo and hi give the same half width
+ * it is exact, and hi is a valid bound for fm_build's proofs (vmax_x/y);
+ * otherwise the caller runs fm_velocity_scan. */
+int32_t fm_velocity_bounds(fm_grid grid, fm_env env, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
+                           double *d_out4, int32_t *d_envelope, void *stream);
+
 /* Segmented max-abs used by velocity_bound (environment.py:404-419):
  * d_out[s] = max_k |src[(s / inner) * outer_stride + (s % inner) * inner_stride
  *                     + k * elem_stride]|, k in [0, seg_len). */

@@ -128,6 +128,8 @@ SIGNATURES = {
                                          C.c_void_p]),
     "fm_velocity_scan": (C.c_int32, [FmGrid, FmEnv, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                      C.c_void_p, C.c_void_p]),
+    "fm_velocity_bounds": (C.c_int32, [FmGrid, FmEnv, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                       C.c_void_p, C.c_void_p]),
     "fm_maxabs_segments": (C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                        C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
     "fm_mask_sat": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),

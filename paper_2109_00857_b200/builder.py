@@ -53,6 +53,8 @@ class DeviceEnv:
     _vmax: tuple | None = None
     _acts: dict = field(default_factory=dict)
     _scan: tuple | None = None   # (device maxima, j_range) of a scan done during upload
+    _bounds_dev: tuple | None = None   # (device lo/hi bounds [4], j_range) of a bounds scan (upload)
+    _vproof: tuple | None = None       # upper bounds of max|v_c| valid for the build's proofs
     envelope: object = None      # int32 [nt][N_c][4] per-cell velocity envelope (fm_velocity_scan)
     _env_rows: tuple | None = None   # rows [j0, j1) whose envelope is current (all layers)
 
@@ -136,7 +138,7 @@ class DeviceEnv:
         dst = {k: torch.empty(v.shape, dtype=dt[k], device=dev) for k, v in src.items()}
         de = cls(grid=grid, mean=dst["mean"], modes=dst["modes"], coeffs=dst["coeffs"], g=dst["g"],
                  mask=dst["mask"], sat=None, n_modes=int(src["modes"].shape[0]), n_real=int(src["coeffs"].shape[1]))
-        out = torch.zeros(2, dtype=torch.float64, device=dev)
+        out = torch.zeros(4, dtype=torch.float64, device=dev)   # fm_velocity_bounds: lo/hi per component
         j0, j1 = j_range if j_range is not None else (0, grid.ny)
         main = torch.cuda.current_stream(dev)
         copy = torch.cuda.Stream(dev)
@@ -154,8 +156,8 @@ class DeviceEnv:
                 ev = torch.cuda.Event()
                 ev.record(copy)
             main.wait_event(ev)
-            _lib.check(lib.fm_velocity_scan(de.fm_grid(), de.fm_env(), int(t0), int(t1), int(j0), int(j1),
-                                            out.data_ptr(), env_ptr, _lib.stream_ptr(main)), "fm_velocity_scan")
+            _lib.check(lib.fm_velocity_bounds(de.fm_grid(), de.fm_env(), int(t0), int(t1), int(j0), int(j1),
+                                              out.data_ptr(), env_ptr, _lib.stream_ptr(main)), "fm_velocity_bounds")
         with torch.cuda.stream(copy):
             dst["g"].copy_(src["g"], non_blocking=True)
             dst["mask"].copy_(src["mask"], non_blocking=True)
@@ -163,7 +165,7 @@ class DeviceEnv:
         for v in dst.values():                       # written on the copy stream, used on main
             v.record_stream(copy)
         de._make_sat()
-        de._scan = (out, tuple(j_range) if j_range is not None else None)
+        de._bounds_dev = (out, tuple(j_range) if j_range is not None else None)
         de._env_rows = (int(j0), int(j1))
         return de
 
@@ -189,6 +191,8 @@ class DeviceEnv:
         self._vmax = None
         self._vbound = {}
         self._scan = None
+        self._bounds_dev = None
+        self._vproof = None
         self._env_rows = None
 
     def velocity_max(self, j_range: tuple | None = None, group=None) -> tuple:
@@ -229,6 +233,54 @@ class DeviceEnv:
             h = out.cpu().numpy()
             self._vmax = (float(h[0]), float(h[1]))
         return self._vmax
+
+    def subgrid(self, f_max: float, buffer: int = 1, j_range: tuple | None = None, group=None) -> SubGridSpec:
+        """compute_subgrid's half widths (model_builder.py:376-399) from the
+        envelope scan's bounds lo <= max|v_c| <= hi (fm_velocity_bounds; the
+        per-cell envelope the build bins against is written on the way):
+        ceil((v + f_max) dt / dx) is monotone in v, so when lo and hi give
+        the same half width it is the exact one, and hi serves the build's
+        proofs (an upper bound suffices there).  Otherwise -- or with a
+        non-finite input -- the exact scan (velocity_max) decides.  With
+        ``j_range`` / ``group``: this rank's strip, combined by all-reduce."""
+        if buffer < 1:
+            raise ContractViolation("buffer must be >= 1")
+        if self._vmax is not None:
+            return subgrid_from_vmax(self._vmax, f_max, self.grid, buffer)
+        torch = _torch()
+        key = tuple(j_range) if j_range is not None else None
+        if self._bounds_dev is not None and self._bounds_dev[1] == key:
+            out = self._bounds_dev[0]
+        else:
+            out = torch.zeros(4, dtype=torch.float64, device=self.mean.device)
+            r0, r1 = (0, self.grid.ny) if j_range is None else (int(j_range[0]), int(j_range[1]))
+            _lib.check(_lib.load().fm_velocity_bounds(self.fm_grid(), self.fm_env(), 0, self.grid.nt, r0, r1,
+                                                      out.data_ptr(), self._envelope_buf().data_ptr(),
+                                                      _lib.stream_ptr()), "fm_velocity_bounds")
+            self._env_rows = (r0, r1)
+        self._bounds_dev = None
+        multi = group is not None or _dist_world() > 1
+        if j_range is not None and multi:
+            from .sharding import all_reduce_max
+            all_reduce_max(out, group)   # non-negative: max of maxima (+inf stays)
+        lox, hix, loy, hiy = (float(x) for x in out.cpu().numpy())
+        if all(math.isfinite(v) for v in (hix, hiy)):
+            lo = subgrid_from_vmax((lox, loy), f_max, self.grid, buffer)
+            hi = subgrid_from_vmax((hix, hiy), f_max, self.grid, buffer)
+            if lo == hi:
+                if j_range is None or multi:   # a strip's bounds alone are not the field's
+                    self._vproof = (hix, hiy)
+                return hi
+        return subgrid_from_vmax(self.velocity_max(j_range=j_range, group=group), f_max, self.grid, buffer)
+
+    def proof_vmax(self) -> tuple:
+        """Upper bounds of max|v_x|, max|v_y| for fm_build's proofs: the exact
+        maxima when known, else the bounds of the last subgrid() call."""
+        if self._vmax is not None:
+            return self._vmax
+        if self._vproof is not None:
+            return self._vproof
+        return self.velocity_max()
 
     def _maxima(self):
         """Device max-abs reductions behind velocity_bound (environment.py:404-419):
@@ -314,14 +366,16 @@ def subgrid_from_vmax(vmax: tuple, f_max: float, grid, buffer: int = 1) -> SubGr
 def compute_subgrid(field, actions, grid, buffer: int = 1, device_env: DeviceEnv | None = None) -> SubGridSpec:
     """Drop-in for model_builder.compute_subgrid (model_builder.py:376-399).
 
-    The exact max over every (t, realization, cell) runs in ``k_vmax``."""
+    The max over every (t, realization, cell) runs in ``k_vmax``: the f32
+    envelope's bounds decide the half widths when unambiguous, else the
+    exact f64 scan (DeviceEnv.subgrid)."""
     if buffer < 1:
         raise ContractViolation("buffer must be >= 1")
     denv = device_env
     if denv is None:
         env = _FieldOnly(grid, field)
         denv = DeviceEnv.from_host(env)
-    return subgrid_from_vmax(denv.velocity_max(), actions.f_max, grid, buffer)
+    return denv.subgrid(actions.f_max, buffer)
 
 
 class _FieldOnly:
@@ -640,7 +694,7 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
                        float(rcfg.r_term), float(rcfg.r_outbound), ti, tj)
     # the exact velocity maxima (when this env's sub-grid scan has run) let
     # the kernel prove the lean path's preconditions; they change no output
-    vmx, vmy = denv.velocity_max() if lean else (-1.0, -1.0)
+    vmx, vmy = denv.proof_vmax() if lean else (-1.0, -1.0)
     recs = np.ascontiguousarray(recs)
     args = _lib.FmBuildArgs(denv.fm_grid(), denv.fm_env(), rw, d_act.data_ptr(), na, hx, hy, 0, 0,
                             denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr(),

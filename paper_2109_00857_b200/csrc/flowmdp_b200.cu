@@ -161,10 +161,13 @@ static void pool_keep()
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------
+// max that keeps a NaN (numpy's max propagates it)
+__device__ __forceinline__ double nan_max(double m, double x) { return (x != x || x > m) ? x : m; }
+
 __device__ __forceinline__ double warp_max_f64(double v)
 {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+    for (int o = 16; o; o >>= 1) v = nan_max(v, __shfl_xor_sync(kFull, v, o));
     return v;
 }
 
@@ -255,7 +258,11 @@ __global__ void k_envelope_init(int4 *vr, int nc, int t0, int nts, int cell0, in
     vr[(size_t)t * nc + c] = make_int4(pinf, ninf, pinf, ninf);
 }
 
-template <int NMX>
+// EXACT: the exact maxima (out2[0..1]); otherwise bounds only (out2[0..3] =
+// lo_x, hi_x, lo_y, hi_y with lo <= max|v_c| <= hi, from the f32 envelope
+// widened by the per-cell error bound; +inf if an input is not finite) and
+// the envelope -- no per-element threshold test, no f64 recompute.
+template <int NMX, bool EXACT = true>
 __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int cell0, int ncell, int r_per_block,
                                                const double *cmax, double *out2, int4 *vrange)
 {
@@ -346,7 +353,7 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
                     for (int q = 0; q < kVmaxCells; ++q) v[j][q] = ffma2_bcast(cj, d32[q][m], v[j][q]);
                 }
             }
-            if (vrange) {
+            if (vrange || !EXACT) {
 #pragma unroll
                 for (int j = 0; j < kVmaxStep; ++j)
 #pragma unroll
@@ -357,6 +364,7 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
                         vhi[q].y = fmaxf(vhi[q].y, v[j][q].y);
                     }
             }
+            if (!EXACT) continue;
             // !(|v| < th) also routes NaN / inf to the exact path
             bool hit = false;
 #pragma unroll
@@ -399,6 +407,31 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
                                __fadd_ru(vhi[q].x, __double2float_ru(delx[q])),
                                __fsub_rd(vlo[q].y, __double2float_ru(dely[q])),
                                __fadd_ru(vhi[q].y, __double2float_ru(dely[q])), gridDim.z == 1);
+    }
+    if constexpr (!EXACT) {
+        double lox = 0.0, hix = 0.0, loy = 0.0, hiy = 0.0;
+#pragma unroll
+        for (int q = 0; q < kVmaxCells; ++q) {
+            if (!ok[q]) continue;
+            const double ax = fmax(-(double)vlo[q].x, (double)vhi[q].x), ay = fmax(-(double)vlo[q].y, (double)vhi[q].y);
+            // a non-finite input (or a bound that is not small) -> +inf: the caller takes the exact scan
+            const bool fin = delx[q] < 1e30 && dely[q] < 1e30;
+            lox = fmax(lox, __dsub_rd(ax, delx[q]));
+            hix = fin ? fmax(hix, __dadd_ru(ax, delx[q])) : __longlong_as_double(0x7ff0000000000000LL);
+            loy = fmax(loy, __dsub_rd(ay, dely[q]));
+            hiy = fin ? fmax(hiy, __dadd_ru(ay, dely[q])) : __longlong_as_double(0x7ff0000000000000LL);
+        }
+        lox = warp_max_f64(lox);
+        hix = warp_max_f64(hix);
+        loy = warp_max_f64(loy);
+        hiy = warp_max_f64(hiy);
+        if ((threadIdx.x & 31) == 0) {
+            atomic_max_nonneg(out2, lox);
+            atomic_max_nonneg(out2 + 1, hix);
+            atomic_max_nonneg(out2 + 2, loy);
+            atomic_max_nonneg(out2 + 3, hiy);
+        }
+        return;
     }
     // non-negative doubles (and +NaN, above +inf) order like their bit patterns
     unsigned long long bx = (unsigned long long)__double_as_longlong(ex),
@@ -502,8 +535,35 @@ extern "C" int32_t fm_velocity_max_rows(fm_grid G, fm_env E, int32_t j0, int32_t
     return fm_velocity_max_slab(G, E, 0, G.nt, j0, j1, d_out2, stream);
 }
 
+static int32_t velocity_scan(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1, double *d_out2,
+                             int32_t *d_envelope, void *stream, bool exact);
+
 extern "C" int32_t fm_velocity_scan(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
                                     double *d_out2, int32_t *d_envelope, void *stream)
+{
+    return velocity_scan(G, E, t0, t1, j0, j1, d_out2, d_envelope, stream, true);
+}
+
+extern "C" int32_t fm_velocity_bounds(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1,
+                                      double *d_out4, int32_t *d_envelope, void *stream)
+{
+    if (E.n_modes > 16) {   // the f64 scan (no f32 envelope): exact maxima as both bounds
+        double *tmp = nullptr;
+        cudaStream_t s = (cudaStream_t)stream;
+        FM_CK(cudaMallocAsync(&tmp, 2 * sizeof(double), s));
+        FM_CK(cudaMemsetAsync(tmp, 0, 2 * sizeof(double), s));
+        const int32_t st = velocity_scan(G, E, t0, t1, j0, j1, tmp, d_envelope, stream, true);
+        if (st != FM_OK) return st;
+        for (int k = 0; k < 4; ++k)
+            FM_CK(cudaMemcpyAsync(d_out4 + k, tmp + k / 2, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        FM_CK(cudaFreeAsync(tmp, s));
+        return FM_OK;
+    }
+    return velocity_scan(G, E, t0, t1, j0, j1, d_out4, d_envelope, stream, false);
+}
+
+static int32_t velocity_scan(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_t j0, int32_t j1, double *d_out2,
+                             int32_t *d_envelope, void *stream, bool exact)
 {
     if (G.nx < 1 || G.ny < 1 || G.nt < 1 || E.n_real < 1 || E.n_modes < 0)
         return fm_fail(FM_BAD_ARG, "fm_velocity_max: bad dims");
@@ -554,7 +614,14 @@ extern "C" int32_t fm_velocity_scan(fm_grid G, fm_env E, int32_t t0, int32_t t1,
                                                                                       j0 * G.nx, nc);
         FM_CK_LAUNCH("k_envelope_init");
     }
-    if (nm <= 4)
+    if (!exact) {
+        if (nm <= 4)
+            k_vmax<4, false><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2, vr);
+        else if (nm <= 8)
+            k_vmax<8, false><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2, vr);
+        else
+            k_vmax<16, false><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2, vr);
+    } else if (nm <= 4)
         k_vmax<4><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2, vr);
     else if (nm <= 8)
         k_vmax<8><<<grid, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpb, cmax, d_out2, vr);
@@ -574,7 +641,7 @@ __global__ void k_maxabs_seg(const double *src, int64_t seg_len, int64_t elem_st
     const int64_t s = blockIdx.x;
     const double *b = src + (s / inner) * outer_stride + (s % inner) * inner_stride;
     double m = 0.0;
-    for (int64_t k = threadIdx.x; k < seg_len; k += blockDim.x) m = fmax(m, fabs(b[k * elem_stride]));
+    for (int64_t k = threadIdx.x; k < seg_len; k += blockDim.x) m = nan_max(m, fabs(b[k * elem_stride]));
     m = warp_max_f64(m);
     __shared__ double red[32];
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -3028,7 +3095,10 @@ static int32_t launch_build_p(const BuildK &K, size_t smem, cudaStream_t s)
     FM_CK(cudaMemsetAsync(K.task_counter, 0, sizeof(unsigned int), s));
     int sms = sm_count() - K.reserve_sms;
     if (sms < 1) sms = 1;
-    kern<<<occ * sms, 32 * wpb, bytes, s>>>(K);
+    // the list launch (tasks the bin-only launches could not bin: usually
+    // none or a few dozen) runs on a small grid -- most of its cost is launch
+    const int blocks = (PART == 0 && K.task_list) ? (sms + 3) / 4 : occ * sms;
+    kern<<<blocks, 32 * wpb, bytes, s>>>(K);
     FM_CK_LAUNCH("k_build");
     return FM_OK;
 }
@@ -3551,24 +3621,44 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
 
 // Bin path inputs for slabs [t0, t1): f32 coefficients padded to 8 modes
 // ([t - t0][r][8]) and max_r |coeff| per (t, m) (the error bound's T).
-__global__ void k_bin_prep(const double *coeffs, int t0, int nts, int nr, int nr_pad, int nm, float *c32, double *cmax)
+// Bin path inputs for slabs [t0, t1): f32 coefficients padded to 8 modes
+// and to nr_pad realizations ([t - t0][r][8]) and max_r |coeff| per (t, m)
+// (the error bound's T).  Block (chunk, t): a grid-stride pass, then one
+// block-level max per mode (8 atomics per block, NaN-sticky).
+__global__ void __launch_bounds__(256) k_bin_prep(const double *coeffs, int t0, int nts, int nr, int nr_pad, int nm,
+                                                  float *c32, double *cmax)
 {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (long long)nts * nr_pad) return;
-    const int tl = (int)(i / nr_pad), r = (int)(i % nr_pad);
-    const double *src = coeffs + ((size_t)(t0 + tl) * nr + r) * nm;
-    float out[8];
+    const int tl = blockIdx.y;
+    const double *base = coeffs + (size_t)(t0 + tl) * nr * nm;
+    double mx[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) mx[m] = 0.0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nr_pad; r += gridDim.x * blockDim.x) {
+        float out[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const double c = (m < nm && r < nr) ? base[(size_t)r * nm + m] : 0.0;
+            out[m] = (float)c;
+            mx[m] = nan_max(mx[m], fabs(c));
+        }
+        float4 *dst = reinterpret_cast<float4 *>(c32 + ((size_t)tl * nr_pad + r) * 8);
+        dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+    }
+    __shared__ double red[8][8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-        const double c = (m < nm && r < nr) ? src[m] : 0.0;
-        out[m] = (float)c;
-        if (m < nm && r < nr)
-            atomicMax(reinterpret_cast<unsigned long long *>(cmax + (size_t)tl * nm + m),
-                      (unsigned long long)__double_as_longlong(fabs(c)));   // non-negative: bits order
+        const double w = warp_max_f64(mx[m]);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][m] = w;
     }
-    float4 *dst = reinterpret_cast<float4 *>(c32 + (size_t)i * 8);
-    dst[0] = make_float4(out[0], out[1], out[2], out[3]);
-    dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+    __syncthreads();
+    if (threadIdx.x < nm && threadIdx.x < 8) {
+        double w = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) w = nan_max(w, red[k][threadIdx.x]);
+        // non-negative doubles (and +NaN) order like their bit patterns
+        atomicMax(reinterpret_cast<unsigned long long *>(cmax + (size_t)tl * nm + threadIdx.x),
+                  (unsigned long long)__double_as_longlong(w));
+    }
 }
 
 extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *stream)
@@ -3589,8 +3679,8 @@ extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *st
         FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&c32), sizeof(float) * 8 * (size_t)nts * K.nr_pad, s));
         FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&cmax), sizeof(double) * (size_t)nts * (K.nm ? K.nm : 1), s));
         FM_CK(cudaMemsetAsync(cmax, 0, sizeof(double) * (size_t)nts * (K.nm ? K.nm : 1), s));
-        const long long n = (long long)nts * K.nr_pad;
-        k_bin_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(K.coeffs, K.t0, nts, K.nr, K.nr_pad, K.nm, c32, cmax);
+        const int bxp = (K.nr_pad + 1023) / 1024;   // 4 realizations per thread
+        k_bin_prep<<<dim3(bxp, nts), 256, 0, s>>>(K.coeffs, K.t0, nts, K.nr, K.nr_pad, K.nm, c32, cmax);
         FM_CK_LAUNCH("k_bin_prep");
         K.coef32 = c32;
         K.cmax = cmax;

@@ -10,7 +10,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .builder import DeviceEnv, build_device_model, subgrid_from_vmax
+from .builder import DeviceEnv, build_device_model
 from .core_types import PolicyValue, SubGridSpec
 from .solver import solve_backward
 
@@ -39,8 +39,7 @@ def plan(env, actions, rcfg, target, buffer: int = 1, device_env: DeviceEnv | No
     reused through ``device_env``."""
     # host inputs: the exact scan runs slab by slab under the upload
     denv = device_env if device_env is not None else DeviceEnv.from_host_scanned(env)
-    sub = subgrid if subgrid is not None else subgrid_from_vmax(denv.velocity_max(), actions.f_max,
-                                                               denv.grid, buffer)
+    sub = subgrid if subgrid is not None else denv.subgrid(actions.f_max, buffer)
     # the solve is queued behind the build; the build's census/overflow
     # check runs once both are in flight (one host round trip)
     dm = build_device_model(denv, actions, rcfg, target, sub, defer_check=True)

@@ -290,16 +290,18 @@ class StripPlanner:
         ``self.sink_bytes`` = the bytes copied."""
         import torch
 
-        from .builder import build_device_model, subgrid_from_vmax
+        from .builder import build_device_model
         de, g = self.denv, self.denv.grid
         if not scanned:
             de.reset_derived()
         ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
         self.events = {"start": ev(), "scanned": ev(), "built": ev(), "solved": ev()}
         self.events["start"].record()
-        vm = de.velocity_max(j_range=(self.j0, self.j1), group=self.group) if self.world > 1 else de.velocity_max()
+        if self.world > 1:
+            sub = de.subgrid(self.actions.f_max, self.buffer, j_range=(self.j0, self.j1), group=self.group)
+        else:
+            sub = de.subgrid(self.actions.f_max, self.buffer)
         self.events["scanned"].record()
-        sub = subgrid_from_vmax(vm, self.actions.f_max, g, self.buffer)
         dm = build_device_model(de, self.actions, self.rcfg, self.target, sub, j_range=(self.j0, self.j1),
                                 defer_check=True, reuse=self.dm, t_groups=slab_groups(g.nt, self.n_groups),
                                 reserve_sms=self.reserve_sms)

@@ -271,6 +271,50 @@ def test_velocity_max_exact(case):
         assert np.float64(got[1]).tobytes() == np.float64(want[1]).tobytes()
 
 
+@pytest.mark.parametrize("case", ["random", "tiny", "smoke", "desk", "paper_1k", "nan"])
+def test_velocity_bounds_and_subgrid(case):
+    """fm_velocity_bounds: lo <= the exact max (the oracle's f64 scan) <= hi
+    per component, and DeviceEnv.subgrid (bounds when they agree, else the
+    exact scan) gives compute_subgrid's half widths (model_builder.py:376-399)
+    for buffers 1 and 2; a NaN input makes hi infinite (the exact scan then
+    propagates the NaN like numpy)."""
+    import math
+    import torch
+    from paper_2109_00857_b200 import _lib, workloads
+    if case == "random":
+        cases = [make_random_env(s) for s in RANDOM_SEEDS]
+        envs = [(c[0], c[1].f_max) for c in cases]
+    elif case == "tiny":
+        envs = [(make_tiny_env(), 1.0)]
+    elif case == "paper_1k":
+        envs = [(workloads.get("paper").with_(n_realizations=1000).environment(), 1.0)]
+    elif case == "nan":
+        import copy
+        env = copy.deepcopy(make_named_env("smoke")[0])
+        env.field.coeffs[3, 5, 2] = np.nan
+        envs = [(env, 1.0)]
+    else:
+        envs = [(make_named_env(case)[0], 1.0)]
+    for env, f_max in envs:
+        de = DeviceEnv.from_host(env)
+        g = env.grid
+        out = torch.zeros(4, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.load().fm_velocity_bounds(de.fm_grid(), de.fm_env(), 0, g.nt, 0, g.ny, out.data_ptr(),
+                                                  de._envelope_buf().data_ptr(), _lib.stream_ptr()), "bounds")
+        lox, hix, loy, hiy = out.cpu().numpy()
+        want = O.velocity_max(env.field)
+        if case == "nan":
+            assert math.isinf(hix) or math.isinf(hiy)
+            continue
+        assert lox <= want[0] <= hix and loy <= want[1] <= hiy
+        for buf in (1, 2):
+            de2 = DeviceEnv.from_host(env)
+            sub = de2.subgrid(f_max, buf)
+            hw = O.compute_subgrid(env.field, f_max, g, buffer=buf) if buf != 1 else O.compute_subgrid(
+                env.field, f_max, g)
+            assert (sub.half_width_x, sub.half_width_y) == tuple(hw)
+
+
 @pytest.mark.parametrize("name", ["desk", "paper"])
 def test_workload_subgrid_hints(name):
     """bench.py's CPU sample uses these pinned sub-grids; the GPU's exact scan must agree."""
