@@ -55,6 +55,9 @@ def _args():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default=WORKLOAD)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--reward-sum", default="sequential", choices=["sequential", "counts"],
+                   help="row rewards: the reference's sequential sum (bit-exact, default) or formed from the "
+                        "per-slot counts (rewards within ~1e-13 relative; north_star tolerance 1e-5)")
     p.add_argument("--reserve-sms", type=int, default=2,
                    help="SMs the build leaves to the pipelined solve stream (with --groups > 1)")
     p.add_argument("--groups", type=int, default=5,
@@ -137,6 +140,13 @@ def config_of(w, world: int, backend: str = "nccl") -> dict:
             "transitions": w.transitions,
             "parallelism": f"ystrips{world}" + ("-gloo-validation" if backend == "gloo" else ""),
             "l2": "flushed between steps (256 MiB write); inputs 185 MB > L2"}
+
+
+def config_with_rewards(cfg: dict, reward_sum: str) -> dict:
+    if reward_sum != "sequential":
+        cfg = dict(cfg, reward_sum=reward_sum + " (rewards within 1e-12 relative of the sequential sum; "
+                                               "counts / columns bit-exact)")
+    return cfg
 
 
 def cpu_baseline(w, env, subgrid=None) -> dict:
@@ -264,7 +274,7 @@ def run_ours(args):
     # solve + halo exchange of each group pipelined on a second stream
     denv = DeviceEnv.from_host(env)
     planner = StripPlanner(denv, acts, rcfg, w.target, w.buffer, n_groups=args.groups,
-                           reserve_sms=args.reserve_sms if args.groups > 1 else 0)
+                           reserve_sms=args.reserve_sms if args.groups > 1 else 0, reward_sum=args.reward_sum)
     j0, j1 = planner.j0, planner.j1
     n_g = g.nx * g.ny * g.nt
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -439,7 +449,7 @@ def run_ours(args):
             "metric": "transitions_per_s", "value": value, "unit": "transitions/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_of(w, world, args.dist_backend),
+            "config": config_with_rewards(config_of(w, world, args.dist_backend), args.reward_sum),
             "stages": {"scan_build_ms_median": build_ms, "scan_ms_median": scan_ms, "k_build_ms_median": kbuild_ms, "solve_exposed_ms_median": solve_ms,
                        "step_ms": ms_per_step, "nnz_rank0": nnz_rank, "strips": planner.bounds,
                        "pipelined_slab_groups": planner.n_groups},

@@ -150,6 +150,14 @@ typedef struct {
      * ends).  Builds whose tasks cannot be told apart (no proven fast path)
      * do everything in the lean phase. */
     int32_t phases;
+    /* Row rewards (model_builder.py:457-458, 462-464): 0 = the reference's
+     * sequential f64 sum over realizations in ascending order (bit-exact;
+     * formed from the counts only when provably exact); 1 = formed from the
+     * per-slot counts (sum over landing slots of count x reward) whenever the
+     * fast path is proven -- counts, columns and probabilities stay
+     * bit-exact, rewards agree to rounding (relative ~1e-13, north_star
+     * allows 1e-5); lets net-energy rows take the binned build. */
+    int32_t reward_mode;
 } fm_build_args;
 
 /* Sub-grid overflow report (message of model_builder.py:433-438). */

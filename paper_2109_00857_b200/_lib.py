@@ -93,7 +93,8 @@ class FmBuildArgs(C.Structure):
                 ("t0", C.c_int32), ("t1", C.c_int32), ("j0", C.c_int32), ("j1", C.c_int32),
                 ("viol_flags", C.c_void_p), ("task_counter", C.c_void_p), ("d_gate_r", C.c_void_p),
                 ("h_actions", C.c_void_p), ("vmax_x", C.c_double), ("vmax_y", C.c_double),
-                ("envelope", C.c_void_p), ("reserve_sms", C.c_int32), ("phases", C.c_int32)]
+                ("envelope", C.c_void_p), ("reserve_sms", C.c_int32), ("phases", C.c_int32),
+                ("reward_mode", C.c_int32)]
 
 
 class FmViolation(C.Structure):

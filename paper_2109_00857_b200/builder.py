@@ -629,8 +629,17 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
                        t_range: tuple | None = None, j_range: tuple | None = None,
                        capacity_hint: int | None = None, defer_check: bool = False,
                        lean: bool = True, reuse: DeviceModel | None = None,
-                       t_groups: list | None = None, reserve_sms: int = 0) -> DeviceModel:
+                       t_groups: list | None = None, reserve_sms: int = 0,
+                       reward_sum: str = "sequential") -> DeviceModel:
     """Run K_build over slabs t_range x row strip j_range; the model stays in HBM.
+
+    ``reward_sum``: "sequential" (default) -- row rewards are the
+    reference's ascending-realization f64 sum (model_builder.py:457-458),
+    bit-exact; "counts" -- formed from the per-slot counts whenever the fast
+    path is proven (fm_build_args.reward_mode 1): counts, columns and
+    probabilities stay bit-exact, rewards agree to rounding (~1e-13
+    relative; north_star's tolerance is 1e-5) and net-energy rows take the
+    binned build.
 
     With defer_check the kernel is only enqueued: consumers (the backward
     solve) can be queued behind it and ``DeviceModel.check()`` performs the
@@ -700,6 +709,9 @@ def build_device_model(denv: DeviceEnv, actions, rcfg, target, subgrid: SubGridS
                             denv.sat.data_ptr(), t0, t1, j0, j1, viol.data_ptr(), counter.data_ptr(),
                             d_gate.data_ptr(), recs.ctypes.data if lean else None, vmx, vmy,
                             denv.envelope_for(j0, j1) if lean else None, int(reserve_sms))
+    if reward_sum not in ("sequential", "counts"):
+        raise ContractViolation(f"reward_sum must be 'sequential' or 'counts', not {reward_sum!r}")
+    args.reward_mode = 1 if reward_sum == "counts" else 0
     if entries is None:
         entries = torch.empty(int(cap), dtype=torch.int32, device=dev)
     dm = DeviceModel(grid=grid, n_actions=na, n_real=denv.n_real, subgrid=subgrid,

@@ -2811,10 +2811,33 @@ __global__ void __launch_bounds__(128, (PART != 0 && (FLAGS & F_PROVEN) && (FLAG
                 // (dead rows: all OUT; the target's rewards are 0.0);
                 // + 0.0 turns a -0.0 into the loop's +0.0
                 const int n_out = h16[nslot * 32], n_hit = R.tslot >= 0 ? h16[R.tslot * 32] : 0;
-                const int n_norm = nr - n_out - n_hit;
-                S = DADD(DADD(DADD(DMUL((double)n_norm, R.base), DMUL((double)n_hit, R.base_hit)),
-                              DMUL((double)n_out, K.r_out)),
-                         0.0);
+                if constexpr ((FLAGS & F_NET) != 0) {
+                    // reward_mode 1 (counts): sum over landing slots, in slot
+                    // order, of count x step_flat's net-energy reward
+                    // ((-(c_f f f) + h_cr g_src + h_cr g_dst) dt, + r_term at
+                    // the target; model_builder.py:357-360) -- agrees with the
+                    // sequential sum to rounding.  Landings outside the domain
+                    // were folded into OUT above.
+                    S = 0.0;
+                    if (!(R.rflags & RF_DEAD)) {
+                        const double *g_n = K.g + (size_t)(t + 1) * K.nc;
+                        for (int sl = 0; sl < nslot; ++sl) {
+                            const int cnt = h16[sl * 32];
+                            if (!cnt) continue;
+                            const int li = R.ci + sl % W - K.hx, lj = R.cj + sl / W - K.hy;
+                            double b = DADD(R.AB, DMUL(K.h_cr, __ldg(g_n + lj * K.nx + li)));
+                            if (!(FLAGS & F_DT_ONE)) b = DMUL(b, K.dt);
+                            if (sl == R.tslot) b = DADD(b, K.r_term);
+                            S = DADD(S, DMUL((double)cnt, b));
+                        }
+                    }
+                    S = DADD(DADD(S, DMUL((double)n_out, K.r_out)), 0.0);
+                } else {
+                    const int n_norm = nr - n_out - n_hit;
+                    S = DADD(DADD(DADD(DMUL((double)n_norm, R.base), DMUL((double)n_hit, R.base_hit)),
+                                  DMUL((double)n_out, K.r_out)),
+                             0.0);
+                }
                 if (R.rflags & RF_TERMINAL) S = 0.0;
             }
         }
@@ -3110,7 +3133,7 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s, int 
         return (phases & 1) ? launch_build_p<FL, 0>(K, smem, s) : FM_OK;   // one class: the lean phase
     } else {
         int32_t st = FM_OK;
-        if constexpr ((FL & F_CNT) != 0 && (FL & F_NET) == 0) {
+        if constexpr ((FL & F_CNT) != 0) {
             if (K.bin_ok && !getenv("FM_NO_BINONLY")) {
                 // bin-only launches (lean, then obstacle tasks); the tasks
                 // they cannot bin run per transition in a PART 0 launch over
@@ -3242,7 +3265,8 @@ static int32_t launch_build(const BuildK &K, int flags, size_t smem, cudaStream_
 #define FM_CASE(F) \
     case F: return launch_build_t<F>(K, smem, s, phases);
             FM_CASE(11 | F_PROVEN) FM_CASE(11 | F_PROVEN | F_CNT) FM_CASE(11 | F_PROVEN | F_NET)
-            FM_CASE(F_PROVEN) FM_CASE(F_PROVEN | F_CNT) FM_CASE(F_PROVEN | F_NET)
+            FM_CASE(11 | F_PROVEN | F_CNT | F_NET)
+            FM_CASE(F_PROVEN) FM_CASE(F_PROVEN | F_CNT) FM_CASE(F_PROVEN | F_NET) FM_CASE(F_PROVEN | F_CNT | F_NET)
 #undef FM_CASE
         }
         return fm_fail(FM_BAD_ARG, "k_build: bad flags %d", flags);
@@ -3601,7 +3625,7 @@ static int32_t build_params(const fm_build_args *h, const fm_model *M, BuildK &K
         const double Ry = (h->vmax_y + ay) * G.dt * (1.0 + 0x1p-40) + 0x1p-40 * my;
         sterbenz_axis(G.nx, G.ox, G.dx, Rx, K.sx_lo, K.sx_hi);
         sterbenz_axis(G.ny, G.oy, G.dx, Ry, K.sy_lo, K.sy_hi);
-        if (K.obj != FM_OBJ_NET_ENERGY && rewards_sum_exactly(h)) flags |= F_CNT;
+        if ((K.obj != FM_OBJ_NET_ENERGY && rewards_sum_exactly(h)) || h->reward_mode == 1) flags |= F_CNT;
     }
     if (K.smem_warp > smem_block_optin()) {
         // the shared histogram does not fit even one warp: global fallback

@@ -240,7 +240,8 @@ class StripPlanner:
     again, and a sub-grid violation on any rank raises on every rank."""
 
     def __init__(self, denv, actions, rcfg, target, buffer: int = 1, group=None, n_groups: int = 5,
-                 reserve_sms: int = 2, w_obst: float = 8.0, bounds: list | None = None):
+                 reserve_sms: int = 2, w_obst: float = 8.0, bounds: list | None = None,
+                 reward_sum: str = "sequential"):
         import torch
         import torch.distributed as dist
 
@@ -256,6 +257,7 @@ class StripPlanner:
         self.bounds = bounds
         self.j0, self.j1 = bounds[self.rank]
         self.n_groups, self.reserve_sms = n_groups, reserve_sms
+        self.reward_sum = reward_sum   # build_device_model: "sequential" (bit-exact) or "counts"
         dev = denv.mean.device
         self.values = torch.zeros(g.nt * g.nx * g.ny + 1, dtype=torch.float64, device=dev)
         self.policy = torch.zeros(g.nt * g.nx * g.ny, dtype=torch.int16, device=dev)
@@ -304,7 +306,7 @@ class StripPlanner:
         self.events["scanned"].record()
         dm = build_device_model(de, self.actions, self.rcfg, self.target, sub, j_range=(self.j0, self.j1),
                                 defer_check=True, reuse=self.dm, t_groups=slab_groups(g.nt, self.n_groups),
-                                reserve_sms=self.reserve_sms)
+                                reserve_sms=self.reserve_sms, reward_sum=self.reward_sum)
         self.dm = dm
         self.events["built"].record()
         self._solve(dm, pipelined=True)

@@ -501,3 +501,33 @@ def test_binned_build_equals_per_transition_build(case, monkeypatch):
     ref = flat(build_device_model(denv, acts, rcfg, target, sub))
     assert binned == ref and tri == ref and lean_only == ref
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("case", ["smoke", "desk", "two_obstacles_1k"])
+def test_reward_sum_counts_net_energy(case):
+    """reward_sum="counts" (fm_build_args.reward_mode 1): net-energy rows
+    take the binned build; every COO block (rows, cols, f64 probabilities)
+    stays bit-identical to the oracle's and every reward agrees with the
+    reference's sequential sum (model_builder.py:457-458) within 1e-12
+    relative (north_star allows 1e-5)."""
+    from paper_2109_00857_b200 import workloads
+    if case == "two_obstacles_1k":
+        w = workloads.get("paper_net_energy").with_(n_realizations=1000)
+        env, acts, rcfg, target = w.environment(), w.actions(), w.reward_config(), w.target
+    else:
+        env, acts, rcfg, target, _ = make_named_env(case)
+        rcfg = type(rcfg)(objective="net_energy", c_f=rcfg.c_f, c_r=rcfg.c_r, r_term=rcfg.r_term,
+                          r_outbound=rcfg.r_outbound)
+    denv = DeviceEnv.from_host(env)
+    sub = fm.compute_subgrid(env.field, acts, env.grid, device_env=denv)
+    om = O.build_model(env, acts, rcfg, target, sub.half_width_x, sub.half_width_y)
+    sm = build_device_model(denv, acts, rcfg, target, sub, reward_sum="counts").to_sparse_model()
+    for a in range(acts.n_actions):
+        for t in range(env.grid.nt):
+            r, c, v = om.blocks[a][t]
+            b = sm.blocks[a][t]
+            assert np.array_equal(b.rows, r) and np.array_equal(b.cols, c) and b.vals.tobytes() == v.tobytes()
+    rel = np.abs(sm.rewards - om.rewards) / np.maximum(np.abs(om.rewards), 1.0)
+    assert rel.max() <= 1e-12
+    seq = build_device_model(denv, acts, rcfg, target, sub).to_sparse_model()
+    assert seq.rewards.tobytes() == om.rewards.tobytes()   # the default stays bit-exact
