@@ -13,7 +13,7 @@ env = w.environment()
 denv = DeviceEnv.from_host(env)
 for _ in range(reps):
     denv.reset_derived()
-    sub = subgrid_from_vmax(denv.velocity_max(), w.f_max, env.grid)
+    sub = denv.subgrid(w.f_max, w.buffer)   # the planner's path: envelope bounds (k_vmax<.., false>)
     dm = build_device_model(denv, w.actions(), w.reward_config(), w.target, sub)
     solve_backward(dm)
 torch.cuda.synchronize()

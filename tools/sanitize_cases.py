@@ -29,7 +29,14 @@ def check(name, env, acts, rcfg, target, **kw):
     dm = build_device_model(denv, acts, rcfg, target, sub, **kw)
     solve_backward(dm)
     om = O.build_model(env, acts, rcfg, target, sub.half_width_x, sub.half_width_y, n_threads=os.cpu_count() or 1)
-    ok = model_digest(dm.to_sparse_model()) == model_digest(om)
+    sm = dm.to_sparse_model()
+    if kw.get("reward_sum") == "counts":   # counts / columns exact, rewards to rounding
+        ok = all(np.array_equal(sm.blocks[a][t].cols, om.blocks[a][t][1]) and
+                 sm.blocks[a][t].vals.tobytes() == om.blocks[a][t][2].tobytes()
+                 for a in range(acts.n_actions) for t in range(env.grid.nt))
+        ok = ok and float(np.max(np.abs(sm.rewards - om.rewards) / np.maximum(np.abs(om.rewards), 1.0))) <= 1e-12
+    else:
+        ok = model_digest(sm) == model_digest(om)
     print(f"{name}: {'bit-exact' if ok else 'MISMATCH'}", flush=True)
     assert ok
 
@@ -40,7 +47,8 @@ def small(name, n_rv=48, nt=6, **kw):
     return w.environment(), w.actions(), w.reward_config(), w.target
 
 
-which = sys.argv[1:] or ["bins", "bins_tri", "lean_pt", "obst", "net", "checked", "ghist"]
+which = sys.argv[1:] or ["bins", "bins_tri", "lean_pt", "obst", "obst_pt", "binonly_off", "net", "net_counts",
+                         "checked", "ghist"]
 for case in which:
     if case == "bins":
         check(case, *small("desk"))
@@ -50,8 +58,18 @@ for case in which:
         os.environ["FM_NO_BINS"] = "1"
         check(case, *small("desk"))
         del os.environ["FM_NO_BINS"]
-    elif case == "obst":
+    elif case == "obst":   # obstacle tasks binned (bin-only launches + list launch)
         check(case, *small("paper_net_energy", objective="time"))
+    elif case == "obst_pt":   # obstacle tasks per transition (deferred exact segment queue)
+        os.environ["FM_NO_OBST_BINS"] = "1"
+        check(case, *small("paper_net_energy", objective="time"))
+        del os.environ["FM_NO_OBST_BINS"]
+    elif case == "binonly_off":   # bins with the inline per-transition fallback (PART 1 / 2)
+        os.environ["FM_NO_BINONLY"] = "1"
+        check(case, *small("paper_net_energy", objective="time"))
+        del os.environ["FM_NO_BINONLY"]
+    elif case == "net_counts":
+        check(case, *small("paper_net_energy"), reward_sum="counts")
     elif case == "net":
         check(case, *small("paper_net_energy"))
     elif case == "checked":
