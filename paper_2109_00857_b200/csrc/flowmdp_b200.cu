@@ -737,7 +737,13 @@ enum : int { RF_DEAD = 1, RF_TERMINAL = 2, RF_GATE = 4, RF_LANDWIN = 8, RF_SEGWI
 static constexpr int kBinNS = 128;    // max buckets per unit interval of frac(z) (bin_ns: 32, 64 or 128)
 static constexpr int kBinRep = 16;    // block-shared copies of each table entry (conflict-free lookups)
 static constexpr int kBinMaxA = 64;   // actions with bin parameters
-static constexpr int kBinRing = 8;    // coefficient chunks in flight (32 realizations each)
+#ifndef FM_BIN_RING
+#define FM_BIN_RING 8
+#endif
+static constexpr int kBinRing = FM_BIN_RING;   // coefficient chunks in flight (32 realizations each)
+#ifndef FM_BIN_WORDS2
+#define FM_BIN_WORDS2 1024   // u32 bin counters per warp for two cells (lean bin-only launch)
+#endif
 static constexpr int kBinQ = 128;     // deferred exact realizations per warp
 // obstacle tasks (bin_task<.., OB = true>): a smaller ring beside (not under)
 // the dense histogram, and a larger queue drained whenever it fills up
@@ -2375,8 +2381,12 @@ static_assert(FM_BUILD_RC <= 64, "chunk_rows_obst_cnt marks deferred realization
 // PART 3 / 4: lean / obstacle tasks by binning only (bin_task); a task that
 // cannot bin is appended to K.task_list and run by a PART 0 launch over the
 // list, so these launches carry no per-transition code (instruction cache).
+#ifndef FM_BUILD_MINB3
+#define FM_BUILD_MINB3 FM_BUILD_MINB1
+#endif
 template <int FLAGS, int PART>
-__global__ void __launch_bounds__(128, (PART != 0 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) ? FM_BUILD_MINB1
+__global__ void __launch_bounds__(128, PART == 3 ? FM_BUILD_MINB3
+                                      : (PART != 0 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) ? FM_BUILD_MINB1
                                                                                               : FM_BUILD_MINB)
     k_build(const __grid_constant__ BuildK K)
 {
@@ -3009,7 +3019,7 @@ static void bin_layout(BuildK &K)
     K.off_bins = 0;
     int words = ((K.smem_warp - uni - q) / 4) & ~31;
     const char *ev = getenv("FM_BIN_WORDS");   // dev override (A/B of the occupancy trade-off)
-    const int floor_words = ev ? atoi(ev) : (K.CW >= 2 ? 1024 : 2048);
+    const int floor_words = ev ? atoi(ev) : (K.CW >= 2 ? FM_BIN_WORDS2 : 2048);
     if (words < floor_words) words = floor_words;
     K.bin_words = words;
     K.off_bdense = align16(words * 4);
@@ -3017,6 +3027,24 @@ static void bin_layout(BuildK &K)
     K.off_bq = K.off_bdense + uni;
     const int end = align16(K.off_bq + q);
     if (end > K.smem_warp) K.smem_warp = end;
+    K.off_block = align16(2 * (K.bin_ns + 1) * kBinRep * (int)sizeof(BinEnt));
+}
+
+// Lean tasks in a bin-only launch (PART 3): bin counters | ring, later the
+// dense histogram | queue, nothing of the per-transition layout but its
+// histogram (horizon tasks), so more warps fit per SM.
+static void bin_layout_lean(BuildK &K)
+{
+    const int ring = kBinRing * 32 * 32, dense = (K.nslot + 1) * 64, q = kBinQ * 4;
+    const int uni = align16(ring > dense ? ring : dense);
+    const int words = K.CW >= 2 ? FM_BIN_WORDS2 : 2048;
+    K.bin_words = words;
+    K.off_bins = 0;
+    K.off_bdense = align16(words * 4);
+    K.off_bring = K.off_bdense;
+    K.off_bq = K.off_bdense + uni;
+    const int end = align16(K.off_bq + q);
+    K.smem_warp = end > align16(dense) ? end : align16(dense);
     K.off_block = align16(2 * (K.bin_ns + 1) * kBinRep * (int)sizeof(BinEnt));
 }
 
@@ -3153,7 +3181,11 @@ static int32_t launch_build_t(const BuildK &K, size_t smem, cudaStream_t s, int 
                 K1.src_a_n = cnt;
                 K1.src_b = nullptr;
                 K1.src_b_n = cnt + 3;   // unused with src_b null
-                if (phases & 1) st = launch_build_p<FL, 3>(K1, smem, s);
+                if (phases & 1) {
+                    BuildK K3 = K1;
+                    bin_layout_lean(K3);
+                    st = launch_build_p<FL, 3>(K3, (size_t)4 * K3.smem_warp, s);
+                }
                 if (st == FM_OK && (phases & 2)) {
                     BuildK K2 = K1;
                     K2.src_a = list + (size_t)K.n_tasks;

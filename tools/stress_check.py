@@ -31,7 +31,7 @@ for it in range(2):
     torch.cuda.synchronize()
     e0, e1, e2, e3 = ev(), ev(), ev(), ev()
     e0.record()
-    sub = subgrid_from_vmax(de.velocity_max(), acts.f_max, g, w.buffer)
+    sub = de.subgrid(acts.f_max, w.buffer)   # envelope bounds (exact scan only if ambiguous)
     e1.record()
     dm = build_device_model(de, acts, rcfg, w.target, sub, defer_check=True, reuse=dm)
     e2.record()
