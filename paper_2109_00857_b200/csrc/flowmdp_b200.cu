@@ -738,11 +738,11 @@ static constexpr int kBinNS = 128;    // max buckets per unit interval of frac(z
 static constexpr int kBinRep = 16;    // block-shared copies of each table entry (conflict-free lookups)
 static constexpr int kBinMaxA = 64;   // actions with bin parameters
 #ifndef FM_BIN_RING
-#define FM_BIN_RING 8
+#define FM_BIN_RING 4   // A/B at C2 with 16 warps/SM: 4 chunks 16.4 ms, 8 chunks (12 warps/SM) 17.4 ms
 #endif
 static constexpr int kBinRing = FM_BIN_RING;   // coefficient chunks in flight (32 realizations each)
 #ifndef FM_BIN_WORDS2
-#define FM_BIN_WORDS2 1024   // u32 bin counters per warp for two cells (lean bin-only launch)
+#define FM_BIN_WORDS2 896    // u32 bin counters per warp for two cells (lean bin-only launch: 4 blocks / SM)
 #endif
 static constexpr int kBinQ = 128;     // deferred exact realizations per warp
 // obstacle tasks (bin_task<.., OB = true>): a smaller ring beside (not under)
@@ -2382,7 +2382,7 @@ static_assert(FM_BUILD_RC <= 64, "chunk_rows_obst_cnt marks deferred realization
 // cannot bin is appended to K.task_list and run by a PART 0 launch over the
 // list, so these launches carry no per-transition code (instruction cache).
 #ifndef FM_BUILD_MINB3
-#define FM_BUILD_MINB3 FM_BUILD_MINB1
+#define FM_BUILD_MINB3 4   // lean bin-only launch: 16 warps / SM (128 registers, no spills)
 #endif
 template <int FLAGS, int PART>
 __global__ void __launch_bounds__(128, PART == 3 ? FM_BUILD_MINB3
