@@ -60,7 +60,11 @@ def _args():
                         "per-slot counts (rewards within ~1e-13 relative; north_star tolerance 1e-5)")
     p.add_argument("--reserve-sms", type=int, default=2,
                    help="SMs the build leaves to the pipelined solve stream (with --groups > 1)")
-    p.add_argument("--groups", type=int, default=5,
+    p.add_argument("--group-ratio", type=float, default=0.6,
+                   help="slab group k (launch order, highest t first) holds a share of the slabs proportional "
+                        "to ratio**k: < 1 shrinks the groups toward t = 0, so less of the solve and of the "
+                        "model's D2H is left after the last group's build")
+    p.add_argument("--groups", type=int, default=6,
                    help="slab groups per build: the solve of a group (and its halo exchange) and the model's "
                         "D2H start while the next group builds")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -274,7 +278,8 @@ def run_ours(args):
     # solve + halo exchange of each group pipelined on a second stream
     denv = DeviceEnv.from_host(env)
     planner = StripPlanner(denv, acts, rcfg, w.target, w.buffer, n_groups=args.groups,
-                           reserve_sms=args.reserve_sms if args.groups > 1 else 0, reward_sum=args.reward_sum)
+                           reserve_sms=args.reserve_sms if args.groups > 1 else 0, reward_sum=args.reward_sum,
+                           group_ratio=args.group_ratio)
     j0, j1 = planner.j0, planner.j1
     n_g = g.nx * g.ny * g.nt
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -452,7 +457,8 @@ def run_ours(args):
             "config": config_with_rewards(config_of(w, world, args.dist_backend), args.reward_sum),
             "stages": {"scan_build_ms_median": build_ms, "scan_ms_median": scan_ms, "k_build_ms_median": kbuild_ms, "solve_exposed_ms_median": solve_ms,
                        "step_ms": ms_per_step, "nnz_rank0": nnz_rank, "strips": planner.bounds,
-                       "pipelined_slab_groups": planner.n_groups},
+                       "pipelined_slab_groups": planner.n_groups,
+                       "slab_group_ratio": planner.group_ratio},
             "e2e": {"value": e2e_value, "unit": "transitions/s", "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h_total, "ms_per_step": e2e_ms / args.steps,
                     "path": "pinned host inputs -> DeviceEnv.from_host_scanned (slab-wise H2D + exact scan) -> "

@@ -921,6 +921,13 @@ __device__ __forceinline__ bool seg_samples_blocked(const BuildK &K, int t, doub
                                                     double p1y)
 {
     const double ddx = DSUB(p1x, p0x), ddy = DSUB(p1y, p0y);
+    if (FLAGS & F_PROVEN) {   // finite: the last sample first (see seg_samples_blocked_win)
+        const int i = floor_magic(to_cell<FLAGS>(DADD(p0x, ddx), K.ox, K.dx, K.inv_dx));
+        const int j = floor_magic(to_cell<FLAGS>(DADD(p0y, ddy), K.oy, K.dx, K.inv_dx));
+        if ((unsigned)i < (unsigned)K.nx && (unsigned)j < (unsigned)K.ny &&
+            __ldg(K.mask + (size_t)t * K.nc + j * K.nx + i))
+            return true;
+    }
     const double len = fm_hypot(ddx, ddy);
     double ns = ceil(DDIV(len, K.half_dx));
     if (!(ns >= 1.0)) ns = 1.0;
@@ -956,6 +963,22 @@ __device__ __forceinline__ bool seg_samples_blocked_win(const BuildK &K, const d
                                                         double p0y, double p1x, double p1y)
 {
     const double ddx = DSUB(p1x, p0x), ddy = DSUB(p1y, p0y);
+    {
+        // the last sample first (frac = min(q / n, 1) = 1 exactly at q = n:
+        // p0 + 1 * delta, environment.py:360-362): the test is an OR over the
+        // samples, so an early exit on it is exact.  Most gated transitions
+        // land on a cell the moving obstacle still covers at t -- they end
+        // here without the hypot and the sample loop.
+        const int i = floor_magic(to_cell<FLAGS>(DADD(p0x, ddx), K.ox, K.dx, K.inv_dx));
+        const int j = floor_magic(to_cell<FLAGS>(DADD(p0y, ddy), K.oy, K.dx, K.inv_dx));
+        if ((unsigned)i < (unsigned)K.nx && (unsigned)j < (unsigned)K.ny) {
+            const int li = i - wi0, lj = j - wj0;
+            if (((unsigned)li < (unsigned)ww && (unsigned)lj < (unsigned)wh)
+                    ? mwin[lj * ww + li] != 0
+                    : __ldg(K.mask + (size_t)t * K.nc + j * K.nx + i) != 0)
+                return true;
+        }
+    }
     const double len = fm_hypot(ddx, ddy);
     // ceil(len / (0.5 dx)): for a power-of-two dx the quotient is an exact
     // scaling, so the product by the reciprocal rounds identically
@@ -1763,7 +1786,7 @@ __device__ __forceinline__ double2 exact_velocity(const BuildK &K, int t, int r,
 template <int FLAGS>
 __device__ __forceinline__ int bin_drain(const BuildK &K, const uint32_t *bq, int qn, int t, int grp,
                                          const RowC &Rf, uint16_t *h16q, unsigned hs_word, int outq, bool row_ok,
-                                         int cs_row, unsigned half_one)
+                                         int cs_row, unsigned half_one, int &q_lo, int &q_hi)
 {
     const int lane = threadIdx.x & 31;
     const int n = qn < 32 ? qn : 32, first = qn - n;
@@ -1782,6 +1805,10 @@ __device__ __forceinline__ int bin_drain(const BuildK &K, const uint32_t *bq, in
             double w;
             const int q = lean_transition<FLAGS, false>(K, Rf, make_double2(vx, vy), nullptr, outq, w);
             hist_inc(h16q, hs_word, q, half_one);
+            if (q != outq) {
+                q_lo = min(q_lo, q);
+                q_hi = max(q_hi, q);
+            }
         }
     }
     __syncwarp();
@@ -2023,8 +2050,17 @@ __device__ __forceinline__ int bin_loop(const BuildK &K, const BinCell *B, const
                     asm("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(ex.x), "=f"(ex.y) : "r"(tabx_s + (8u * kBinRep) * (unsigned)__float_as_int(tb.x)));
                     asm("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(ey.x), "=f"(ey.y) : "r"(taby_s + (8u * kBinRep) * (unsigned)__float_as_int(tb.y)));
                     // sign bits: f < lo (below the zone), f > hi (above it)
+#ifndef FM_ZONE_PACKED
+                    // scalar subtractions: no register moves to pair the table halves
+                    float2 dlo, dhi;
+                    asm("sub.rn.f32 %0, %1, %2;" : "=f"(dlo.x) : "f"(f.x), "f"(ex.x));
+                    asm("sub.rn.f32 %0, %1, %2;" : "=f"(dlo.y) : "f"(f.y), "f"(ey.x));
+                    asm("sub.rn.f32 %0, %1, %2;" : "=f"(dhi.x) : "f"(ex.y), "f"(f.x));
+                    asm("sub.rn.f32 %0, %1, %2;" : "=f"(dhi.y) : "f"(ey.y), "f"(f.y));
+#else
                     const float2 dlo = f2_sub(f, make_float2(ex.x, ey.x));
                     const float2 dhi = f2_sub(make_float2(ex.y, ey.y), f);
+#endif
                     const unsigned sx = (unsigned)__float_as_int(dhi.x) >> 31, sy = (unsigned)__float_as_int(dhi.y) >> 31;
                     const unsigned bx = (unsigned)__float_as_int(t1.x) * (unsigned)k1x + cx[q] +
                                         ((unsigned)__float_as_int(ex.x) & 63u) + sx;
@@ -2100,7 +2136,7 @@ __device__ __forceinline__ int floordiv_pos(int a, int b) { return a >= 0 ? a / 
 template <int FLAGS, bool OB>
 __device__ __forceinline__ bool bin_task(const BuildK *__restrict__ Kg, unsigned char *wbase, const BinEnt *tab_s, int t,
                                          int grp, int ag, const RowC &Rf, int outq, bool row_ok, int cs_row,
-                                         unsigned half_one, const uint32_t *danger)
+                                         unsigned half_one, const uint32_t *danger, int &q_lo, int &q_hi)
 {
     const BuildK &K = *Kg;
     const int lane = threadIdx.x & 31;
@@ -2152,7 +2188,7 @@ __device__ __forceinline__ bool bin_task(const BuildK *__restrict__ Kg, unsigned
 #endif
         for (int n = qn; n > 0;) {
             if (OB) n = bin_drain_obst<FLAGS>(K, bq, bins, n, t, grp, ag, dense_s, danger, CWD, db, ftab_s, mwin);
-            else n = bin_drain<FLAGS>(K, bq, n, t, grp, Rf, h16q, hs_word, outq, live_row, cs_row, half_one);
+            else n = bin_drain<FLAGS>(K, bq, n, t, grp, Rf, h16q, hs_word, outq, live_row, cs_row, half_one, q_lo, q_hi);
         }
 #ifdef FM_STATS
         if (OB && lane == 0)
@@ -2339,6 +2375,8 @@ __device__ __forceinline__ bool bin_task(const BuildK *__restrict__ Kg, unsigned
                                              : "memory");
                             } else {
                                 h16q[qq * 32] += (uint16_t)cnt;
+                                q_lo = min(q_lo, qq);
+                                q_hi = max(q_hi, qq);
                             }
                         } else {
                             atomicOr(K.viol + (size_t)t * K.na + a, 2u);   // cannot happen: flags a bug loudly
@@ -2525,6 +2563,10 @@ __global__ void __launch_bounds__(128, PART == 3 ? FM_BUILD_MINB3
                                          R.cj + K.hy >= K.ny);
         double S = 0.0;
         int viol = 0;
+        // slots [s_lo, s_hi] (+ OUT) hold this row's nonzero counts: a lean
+        // binned task narrows it to the slots its counts went to, so the
+        // census and the fill below skip the window's empty slots
+        int s_lo = 0, s_hi = nslot - 1;
         if (PART != 0) {
             const bool obst_task =
                 !horizon && __any_sync(kFull, row_ok && (R.rflags & (RF_DEAD | RF_SEGWIN | RF_LANDWIN)));
@@ -2577,8 +2619,12 @@ __global__ void __launch_bounds__(128, PART == 3 ? FM_BUILD_MINB3
                                 c = (!K.src_cell_exact || box_count(K, t, min(cci, li), max(cci, li),
                                                                     min(ccj, lj), max(ccj, lj)) > 0) ? 2 : 3;
                                 // ex == x1 exactly for this source: the tight box is the exact one
-                                if (c == 3 && (cci >= K.sx_lo || cci <= K.sx_hi) && (ccj >= K.sy_lo || ccj <= K.sy_hi))
-                                    c = 0;
+                                const bool ex_exact = (cci >= K.sx_lo || cci <= K.sx_hi) && (ccj >= K.sy_lo || ccj <= K.sy_hi);
+                                if (c == 3 && ex_exact) c = 0;
+                                // the landing cell itself masked at t: the last sample (frac = 1)
+                                // is ex = x1 (Sterbenz), inside it -- every transition landing
+                                // here is blocked (environment.py:359-367): settled as class 1
+                                if (ex_exact && K.mask[(size_t)t * K.nc + lj * K.nx + li]) c = 1;
                             }
                         }
                     }
@@ -2609,8 +2655,14 @@ __global__ void __launch_bounds__(128, PART == 3 ? FM_BUILD_MINB3
             bool binned = false;
             if constexpr (PART != 0 && (FLAGS & F_PROVEN) && (FLAGS & F_CNT)) {
                 if (K.bin_ok) {
+                    int q_lo = INT_MAX, q_hi = INT_MIN;   // q coordinates (slot - soff), OUT excluded
                     binned = bin_task<FLAGS, OBST_PART>(Kg, wbase, tab_s, t, grp, ag, Rf, outq, row_ok, cs_row,
-                                                        half_one, danger);
+                                                        half_one, danger, q_lo, q_hi);
+                    if (LEAN_PART && binned) {
+                        const bool any = q_lo <= q_hi;   // else every count is OUT
+                        s_lo = any ? q_lo + R.soff : nslot;
+                        s_hi = any ? q_hi + R.soff : nslot - 1;
+                    }
 #ifdef FM_STATS
                     tpath = binned ? 1 : 2;
 #endif
@@ -2870,8 +2922,10 @@ __global__ void __launch_bounds__(128, PART == 3 ? FM_BUILD_MINB3
 
         // ---- emit: nnz census, warp scan, bump allocation, slot-ordered fill
         int nnz = 0;
-        if (row_ok)
-            for (int sl = 0; sl <= nslot; ++sl) nnz += h16[sl * 32] != 0;
+        if (row_ok) {
+            for (int sl = s_lo; sl <= s_hi; ++sl) nnz += h16[sl * 32] != 0;
+            nnz += h16[nslot * 32] != 0;   // OUT
+        }
         int incl = nnz;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -2888,7 +2942,8 @@ __global__ void __launch_bounds__(128, PART == 3 ? FM_BUILD_MINB3
             K.row_ptr[row] = pos;
             K.row_nnz[row] = (uint16_t)nnz;
             K.reward[row] = DDIV(S, (double)nr);   // finalize_rewards (model_builder.py:462-464)
-            for (int sl = 0; sl <= nslot; ++sl) {
+            for (int sl = s_lo; sl <= nslot; ++sl) {
+                if (sl == s_hi + 1) sl = nslot;   // past the range: the OUT slot
                 const uint32_t x = h16[sl * 32];
                 if (!x) continue;
                 h16[sl * 32] = 0;

@@ -220,12 +220,31 @@ def device_solve_sharded(dmodel, values, policy, j0: int, j1: int, group=None, b
     return solve_sharded(layer, values, g.nt, g.nx, g.ny, dmodel.subgrid.half_width_y, group, bounds)
 
 
-def slab_groups(nt: int, n_groups: int) -> list:
+def slab_groups(nt: int, n_groups: int, ratio: float = 1.0) -> list:
     """Descending slab groups [(t0, t1), ...] covering [0, nt), the last
-    layers first (the backward solve's order)."""
+    layers first (the backward solve's order).  Group k (in launch order)
+    gets a share of the slabs proportional to ratio**k: with ratio < 1 the
+    groups shrink toward t = 0, so the work left after the last group's
+    build -- its layers' solve and its share of the model's device-to-host
+    copy -- is small.  Every group holds at least one slab."""
     n = max(1, min(n_groups, nt))
-    cuts = [nt * k // n for k in range(n + 1)]
-    return [(cuts[k], cuts[k + 1]) for k in range(n - 1, -1, -1) if cuts[k] < cuts[k + 1]]
+    if not ratio > 0.0:
+        raise ValueError("ratio must be > 0")
+    w = [ratio ** k for k in range(n)]   # launch order: highest t first
+    tot = sum(w)
+    sizes, acc, done = [], 0.0, 0
+    for k in range(n):
+        acc += w[k]
+        end = nt if k == n - 1 else int(round(nt * acc / tot))
+        end = max(end, done + 1)             # >= 1 slab per group
+        end = min(end, nt - (n - 1 - k))     # leave >= 1 slab for each later group
+        sizes.append(end - done)
+        done = end
+    out, hi = [], nt
+    for sz in sizes:
+        out.append((hi - sz, hi))
+        hi -= sz
+    return out
 
 
 class StripPlanner:
@@ -239,9 +258,9 @@ class StripPlanner:
     is collective: if any rank had to rebuild (capacity) all ranks solve
     again, and a sub-grid violation on any rank raises on every rank."""
 
-    def __init__(self, denv, actions, rcfg, target, buffer: int = 1, group=None, n_groups: int = 5,
+    def __init__(self, denv, actions, rcfg, target, buffer: int = 1, group=None, n_groups: int = 6,
                  reserve_sms: int = 2, w_obst: float = 8.0, bounds: list | None = None,
-                 reward_sum: str = "sequential"):
+                 reward_sum: str = "sequential", group_ratio: float = 0.6):
         import torch
         import torch.distributed as dist
 
@@ -257,6 +276,7 @@ class StripPlanner:
         self.bounds = bounds
         self.j0, self.j1 = bounds[self.rank]
         self.n_groups, self.reserve_sms = n_groups, reserve_sms
+        self.group_ratio = group_ratio
         self.reward_sum = reward_sum   # build_device_model: "sequential" (bit-exact) or "counts"
         dev = denv.mean.device
         self.values = torch.zeros(g.nt * g.nx * g.ny + 1, dtype=torch.float64, device=dev)
@@ -265,14 +285,22 @@ class StripPlanner:
         self.dm = None
         self.events = {}
 
-    def _solve(self, dm, pipelined: bool):
+    def _solve(self, dm, pipelined: bool, after=None):
         import torch
         g = dm.grid
         hy = dm.subgrid.half_width_y
         main = torch.cuda.current_stream()
         ss = self.solve_stream if pipelined else main
         if pipelined:
-            ss.wait_stream(main)   # the values / model buffers of this step
+            # the main-stream work before this step's build (``after``: an
+            # event recorded ahead of the build launches -- waiting on the
+            # main stream itself here would wait for the whole build and
+            # serialise the solve behind it); each group's layers then wait
+            # for that group's build event below
+            if after is not None:
+                ss.wait_event(after)
+            else:
+                ss.wait_stream(main)
         with torch.cuda.stream(ss):
             self.values[-1:].zero_()
             layer = _solve_layer_fn(dm, self.values, self.policy, self.j0, self.j1)
@@ -305,11 +333,11 @@ class StripPlanner:
             sub = de.subgrid(self.actions.f_max, self.buffer)
         self.events["scanned"].record()
         dm = build_device_model(de, self.actions, self.rcfg, self.target, sub, j_range=(self.j0, self.j1),
-                                defer_check=True, reuse=self.dm, t_groups=slab_groups(g.nt, self.n_groups),
+                                defer_check=True, reuse=self.dm, t_groups=slab_groups(g.nt, self.n_groups, self.group_ratio),
                                 reserve_sms=self.reserve_sms, reward_sum=self.reward_sum)
         self.dm = dm
         self.events["built"].record()
-        self._solve(dm, pipelined=True)
+        self._solve(dm, pipelined=True, after=self.events["scanned"])
         self.events["solved"].record()
         self.sink_bytes = 0
         if sink is not None:

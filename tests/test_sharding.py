@@ -147,3 +147,21 @@ def test_halo_plan_with_uneven_bounds():
                 got |= set(range(a, b))
                 assert (r, a, b) in plans[peer][0]   # the peer sends exactly these rows
             assert got == need
+
+
+@pytest.mark.parametrize("nt,n,ratio", [(100, 5, 1.0), (100, 5, 0.7), (100, 6, 0.6), (7, 5, 0.5), (3, 8, 1.0),
+                                        (10, 4, 0.3), (200, 5, 1.3)])
+def test_slab_groups_partition_descending(nt, n, ratio):
+    """The pipelined build's slab groups: a descending partition of [0, nt)
+    with every group non-empty; ratio < 1 makes the last groups smaller."""
+    from paper_2109_00857_b200.sharding import slab_groups
+    gs = slab_groups(nt, n, ratio)
+    assert len(gs) == min(n, nt)
+    assert gs[0][1] == nt and gs[-1][0] == 0
+    assert all(a < b for a, b in gs)
+    assert all(gs[k][0] == gs[k + 1][1] for k in range(len(gs) - 1))
+    sizes = [b - a for a, b in gs]
+    if ratio < 1.0 and nt >= 10 * n:
+        assert sizes[-1] < sizes[0]
+    if ratio == 1.0:
+        assert max(sizes) - min(sizes) <= 1
