@@ -453,6 +453,169 @@ __global__ void __launch_bounds__(256) k_vmax(fm_grid G, fm_env E, int t0, int c
 __global__ void k_maxabs_seg(const double *src, int64_t seg_len, int64_t elem_stride, int64_t inner,
                              int64_t outer_stride, int64_t inner_stride, double *out);
 
+// ---------------------------------------------------------------------------
+// k_vmax_tc: the bounds-only envelope scan (k_vmax<8, false>) with the
+// coefficient x mode contraction on the tensor cores (north_star: "tensor
+// cores for that contraction only if it holds tolerance").  Per warp and
+// step: 16 realizations x 4 cells x (vx, vy) = one m16n8k8 TF32 MMA tile
+// (A = coefficients [realization][mode], B = modes [mode][cell, component],
+// C = mean), run as 3xTF32 (A_lo B_hi + A_hi B_lo + A_hi B_hi: the
+// operands split into two TF32 halves, 2^-22 relative each) so the result
+// carries ~f32 accuracy.  The envelope and the bounds only need a rigorous
+// outer bound, never the f32 value itself: |v_tc - v64| <= delta_tc =
+// 2^-16 T + abs, T = |mean| + sum_m |mode_m| max_r |coeff_m| -- the split
+// (3 * 2^-22 per product) and up to 64 ulps of f32 accumulation error
+// (truncating adds included) are < 2^-17 T, so the factor 2 is slack.
+// (The build's bins only need the envelope as a box hint: a realization
+// outside it takes the exact path, bin_setup.)  Lanes: g = lane >> 2 (row
+// of the tile: realizations g, g + 8), q = lane & 3 (the tile's cell, and
+// the modes q, q + 4 of the A / B fragments).  Environment.py:293-297
+// (reconstruction), model_builder.py:376-399 (the maxima it bounds).
+// ---------------------------------------------------------------------------
+static constexpr int kTcQuads = 2;      // 4-cell tiles per warp (independent MMA chains)
+static constexpr int kTcChunk = 64;     // realizations staged per block step (4 MMA steps)
+
+__device__ __forceinline__ unsigned tf32_rna(float x)
+{
+    unsigned r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1)
+{
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(256) k_vmax_tc(fm_grid G, fm_env E, int t0, int cell0, int ncell, int r_per_block,
+                                                 const double *cmax, double *out4, int4 *vrange)
+{
+    // [step][lane] fragments: (a0, a1, a2, a3) hi, then lo
+    __shared__ uint4 cs_hi[kTcChunk / 16][32], cs_lo[kTcChunk / 16][32];
+    const int nc = G.nx * G.ny, nm = E.n_modes;
+    const int t = t0 + blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+    const int r_lo = blockIdx.z * r_per_block, r_hi = min(E.n_real, r_lo + r_per_block);
+    // this lane's tile column (cell, component) for B, and its D cell
+    unsigned bh0[kTcQuads], bh1[kTcQuads], bl0[kTcQuads], bl1[kTcQuads];
+    float mux[kTcQuads], muy[kTcQuads];
+    float2 vlo[kTcQuads], vhi[kTcQuads];
+    int cell[kTcQuads];
+    bool ok[kTcQuads];
+    double dx_[kTcQuads], dy_[kTcQuads];
+#pragma unroll
+    for (int u = 0; u < kTcQuads; ++u) {
+        const int tile = (blockIdx.x * (blockDim.x >> 5) + warp) * kTcQuads + u;
+        // B column n = g: cell 4 tile + (g >> 1), component g & 1
+        const int lb = tile * 4 + (g >> 1), cb = cell0 + lb;
+        float m0 = 0.f, m1 = 0.f;
+        if (lb < ncell) {
+            if (q < nm) m0 = (float)E.modes[(((size_t)q * G.nt + t) * nc + cb) * 2 + (g & 1)];
+            if (q + 4 < nm) m1 = (float)E.modes[(((size_t)(q + 4) * G.nt + t) * nc + cb) * 2 + (g & 1)];
+        }
+        bh0[u] = tf32_rna(m0);
+        bh1[u] = tf32_rna(m1);
+        bl0[u] = tf32_rna(m0 - __uint_as_float(bh0[u]));
+        bl1[u] = tf32_rna(m1 - __uint_as_float(bh1[u]));
+        // D cell: 4 tile + q
+        const int ld = tile * 4 + q, cd = cell0 + ld;
+        ok[u] = ld < ncell;
+        cell[u] = cd;
+        mux[u] = muy[u] = 0.f;
+        double Tx = 0.0, Ty = 0.0;
+        if (ok[u]) {
+            const double2 mu = *reinterpret_cast<const double2 *>(E.mean + ((size_t)t * nc + cd) * 2);
+            mux[u] = (float)mu.x;
+            muy[u] = (float)mu.y;
+            Tx = fabs(mu.x);
+            Ty = fabs(mu.y);
+            for (int m = 0; m < nm; ++m) {
+                const double2 md = *reinterpret_cast<const double2 *>(E.modes + (((size_t)m * G.nt + t) * nc + cd) * 2);
+                const double cm = cmax[(size_t)(t - t0) * nm + m];
+                Tx += fabs(md.x) * cm;
+                Ty += fabs(md.y) * cm;
+            }
+        }
+        const double kRel = 0x1p-16, kAbs = (nm + 2.0) * 0x1p-140;
+        dx_[u] = Tx * kRel + kAbs;
+        dy_[u] = Ty * kRel + kAbs;
+        vlo[u] = make_float2(__int_as_float(0x7f800000), __int_as_float(0x7f800000));
+        vhi[u] = make_float2(__int_as_float(0xff800000), __int_as_float(0xff800000));
+    }
+    for (int r0 = r_lo; r0 < r_hi; r0 += kTcChunk) {
+        const int n = min(kTcChunk, r_hi - r0);
+        __syncthreads();
+        // stage the chunk as split TF32 fragments (a realization past the
+        // end repeats the last one: harmless for a min / max)
+        for (int i = threadIdx.x; i < kTcChunk * 8; i += blockDim.x) {
+            const int k = i >> 3, m = i & 7;
+            const int kk = min(k, n - 1);
+            const float c = m < nm ? (float)E.coeffs[((size_t)t * E.n_real + r0 + kk) * nm + m] : 0.f;
+            const unsigned h = tf32_rna(c), l = tf32_rna(c - __uint_as_float(h));
+            const int st = k >> 4, rl = k & 15;
+            const int ln = (rl & 7) * 4 + (m & 3), sl = (rl >> 3) + 2 * (m >> 2);
+            reinterpret_cast<unsigned *>(&cs_hi[st][ln])[sl] = h;
+            reinterpret_cast<unsigned *>(&cs_lo[st][ln])[sl] = l;
+        }
+        __syncthreads();
+        for (int st = 0; st < (n + 15) >> 4; ++st) {
+            const uint4 H = cs_hi[st][lane], L = cs_lo[st][lane];
+            const unsigned ah[4] = {H.x, H.y, H.z, H.w}, al[4] = {L.x, L.y, L.z, L.w};
+#pragma unroll
+            for (int u = 0; u < kTcQuads; ++u) {
+                float d[4] = {mux[u], muy[u], mux[u], muy[u]};
+                mma_tf32(d, al, bh0[u], bh1[u]);
+                mma_tf32(d, ah, bl0[u], bl1[u]);
+                mma_tf32(d, ah, bh0[u], bh1[u]);
+                vlo[u].x = fminf(vlo[u].x, fminf(d[0], d[2]));
+                vhi[u].x = fmaxf(vhi[u].x, fmaxf(d[0], d[2]));
+                vlo[u].y = fminf(vlo[u].y, fminf(d[1], d[3]));
+                vhi[u].y = fmaxf(vhi[u].y, fmaxf(d[1], d[3]));
+            }
+        }
+    }
+    double lox = 0.0, hix = 0.0, loy = 0.0, hiy = 0.0;
+#pragma unroll
+    for (int u = 0; u < kTcQuads; ++u) {
+        // the tile's rows: lanes with the same q (xor over the g bits)
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            vlo[u].x = fminf(vlo[u].x, __shfl_xor_sync(kFull, vlo[u].x, o));
+            vhi[u].x = fmaxf(vhi[u].x, __shfl_xor_sync(kFull, vhi[u].x, o));
+            vlo[u].y = fminf(vlo[u].y, __shfl_xor_sync(kFull, vlo[u].y, o));
+            vhi[u].y = fmaxf(vhi[u].y, __shfl_xor_sync(kFull, vhi[u].y, o));
+        }
+        if (g == 0 && ok[u]) {
+            if (vrange)
+                store_envelope(vrange, (size_t)t * nc + cell[u], __fsub_rd(vlo[u].x, __double2float_ru(dx_[u])),
+                               __fadd_ru(vhi[u].x, __double2float_ru(dx_[u])),
+                               __fsub_rd(vlo[u].y, __double2float_ru(dy_[u])),
+                               __fadd_ru(vhi[u].y, __double2float_ru(dy_[u])), gridDim.z == 1);
+            const double ax = fmax(-(double)vlo[u].x, (double)vhi[u].x), ay = fmax(-(double)vlo[u].y, (double)vhi[u].y);
+            // a non-finite input (or a bound that is not small) -> +inf: the caller takes the exact scan
+            const bool fin = dx_[u] < 1e30 && dy_[u] < 1e30;
+            lox = fmax(lox, __dsub_rd(ax, dx_[u]));
+            hix = fin ? fmax(hix, __dadd_ru(ax, dx_[u])) : __longlong_as_double(0x7ff0000000000000LL);
+            loy = fmax(loy, __dsub_rd(ay, dy_[u]));
+            hiy = fin ? fmax(hiy, __dadd_ru(ay, dy_[u])) : __longlong_as_double(0x7ff0000000000000LL);
+        }
+    }
+    lox = warp_max_f64(lox);
+    hix = warp_max_f64(hix);
+    loy = warp_max_f64(loy);
+    hiy = warp_max_f64(hiy);
+    if (lane == 0) {
+        atomic_max_nonneg(out4, lox);
+        atomic_max_nonneg(out4 + 1, hix);
+        atomic_max_nonneg(out4 + 2, loy);
+        atomic_max_nonneg(out4 + 3, hiy);
+    }
+}
+
+
 // More than 16 modes: the plain f64 scan (the filter's per-cell mode
 // registers would not fit).  One thread per cell, RB realizations at a time,
 // modes outer so each mode is loaded once per block of realizations; every
@@ -598,6 +761,33 @@ static int32_t velocity_scan(fm_grid G, fm_env E, int32_t t0, int32_t t1, int32_
         k_maxabs_seg<<<nts * nm, 256, 0, s>>>(E.coeffs + (size_t)t0 * E.n_real * nm, E.n_real, nm, nm,
                                               (int64_t)E.n_real * nm, 1, cmax);
         FM_CK_LAUNCH("k_maxabs_seg");
+    }
+    if (!exact && nm <= 8 && getenv("FM_TC_SCAN")) {
+        // bounds + envelope on the tensor cores (k_vmax_tc, opt-in): 64 cells
+        // per block.  Measured at C2 (one B200): 4.23 ms vs 4.05 ms for the
+        // FFMA2 scan -- the legacy mma.sync TF32 path issues ~1 m16n8k8 per
+        // 21 cycles per SMSP, so the 3xTF32 split costs as much as the FFMA2
+        // chains it replaces; the FFMA2 scan stays the default (its bound is
+        // also 10x tighter)
+        const int cpb = 8 * kTcQuads * 4;
+        const int bxt = (nc + cpb - 1) / cpb;
+        const long long baset = (long long)bxt * nts, wantt = 8LL * sm_count();
+        int rpbt = E.n_real;
+        if (baset < wantt) {
+            const long long split = (wantt + baset - 1) / baset;
+            rpbt = (int)((E.n_real + split - 1) / split);
+            rpbt = ((rpbt + kTcChunk - 1) / kTcChunk) * kTcChunk;
+        }
+        const dim3 gridt(bxt, nts, (E.n_real + rpbt - 1) / rpbt);
+        if (vr && gridt.z > 1) {
+            k_envelope_init<<<(unsigned)(((long long)nts * nc + 255) / 256), 256, 0, s>>>(vr, G.nx * G.ny, t0, nts,
+                                                                                          j0 * G.nx, nc);
+            FM_CK_LAUNCH("k_envelope_init");
+        }
+        k_vmax_tc<<<gridt, 256, 0, s>>>(G, E, t0, j0 * G.nx, nc, rpbt, cmax, d_out2, vr);
+        FM_CK_LAUNCH("k_vmax_tc");
+        FM_CK(cudaFreeAsync(cmax, s));
+        return FM_OK;
     }
     const int bx = (nc + 256 * kVmaxCells - 1) / (256 * kVmaxCells);
     long long base = (long long)bx * nts;

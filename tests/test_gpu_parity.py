@@ -315,6 +315,55 @@ def test_velocity_bounds_and_subgrid(case):
             assert (sub.half_width_x, sub.half_width_y) == tuple(hw)
 
 
+def _decode_envelope(e):
+    """int4 order-preserving f32 encodings -> float64 (lo_x, hi_x, lo_y, hi_y)."""
+    e = e.astype(np.int64)
+    b = np.where(e >= 0, e, e ^ 0x7FFFFFFF).astype(np.uint32)
+    return b.view(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("case,scan", [("desk", "tc"), ("desk", "ffma2"), ("random", "tc"), ("random", "ffma2"),
+                                       ("smoke", "tc")])
+def test_envelope_contains_exact_velocities(case, scan, monkeypatch):
+    """The per-(t, cell) envelope of the bounds scan -- the FFMA2 kernel
+    (k_vmax<.., false>, default) or the tensor-core 3xTF32 one (k_vmax_tc,
+    FM_TC_SCAN=1) -- contains
+    every exact f64 velocity (environment.py:293-297, reference order) and is
+    tight (widening well below a cell); its bounds bracket the exact maxima."""
+    import torch
+    from paper_2109_00857_b200 import _lib
+    if scan == "tc":
+        monkeypatch.setenv("FM_TC_SCAN", "1")
+    else:
+        monkeypatch.delenv("FM_TC_SCAN", raising=False)
+    envs = [make_random_env(s)[0] for s in RANDOM_SEEDS[:6]] if case == "random" else [make_named_env(case)[0]]
+    for env in envs:
+        de = DeviceEnv.from_host(env)
+        g = env.grid
+        out = torch.zeros(4, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.load().fm_velocity_bounds(de.fm_grid(), de.fm_env(), 0, g.nt, 0, g.ny, out.data_ptr(),
+                                                  de._envelope_buf().data_ptr(), _lib.stream_ptr()), "bounds")
+        env_d = _decode_envelope(de._envelope_buf().cpu().numpy())          # [nt][nc][4]
+        F = env.field
+        nt, nc = g.nt, g.nx * g.ny
+        mean = np.asarray(F.mean, np.float64).reshape(nt, nc, 2)
+        modes = np.asarray(F.modes, np.float64).reshape(-1, nt, nc, 2)
+        coeffs = np.asarray(F.coeffs, np.float64)
+        for t in range(nt):
+            v = np.broadcast_to(mean[t][None], (coeffs.shape[1], nc, 2)).copy()
+            for m in range(modes.shape[0]):   # v = v + c_m * mode_m, ascending m (the reference's order)
+                v = v + coeffs[t, :, m][:, None, None] * modes[m, t][None]
+            lo, hi = v.min(axis=0), v.max(axis=0)                          # [nc][2]
+            e = env_d[t]
+            assert np.all(e[:, 0] <= lo[:, 0]) and np.all(hi[:, 0] <= e[:, 1]), (case, t)
+            assert np.all(e[:, 2] <= lo[:, 1]) and np.all(hi[:, 1] <= e[:, 3]), (case, t)
+            assert np.all(e[:, 1] - e[:, 0] - (hi[:, 0] - lo[:, 0]) <= 1e-3 * (1.0 + np.abs(hi[:, 0]) + np.abs(lo[:, 0])))
+            assert np.all(e[:, 3] - e[:, 2] - (hi[:, 1] - lo[:, 1]) <= 1e-3 * (1.0 + np.abs(hi[:, 1]) + np.abs(lo[:, 1])))
+        lox, hix, loy, hiy = out.cpu().numpy()
+        want = O.velocity_max(env.field)
+        assert lox <= want[0] <= hix and loy <= want[1] <= hiy
+
+
 @pytest.mark.parametrize("name", ["desk", "paper"])
 def test_workload_subgrid_hints(name):
     """bench.py's CPU sample uses these pinned sub-grids; the GPU's exact scan must agree."""
