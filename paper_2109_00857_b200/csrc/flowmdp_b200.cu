@@ -1909,23 +1909,27 @@ __device__ __forceinline__ bool bin_setup(const BuildK &K, int t, int c, BinCell
     const size_t cell = (size_t)t * K.nc + c;
     const double2 mu = *reinterpret_cast<const double2 *>(K.mean + cell * 2);
     const double *cm = K.cmax + (size_t)(t - K.t0) * K.nm;
+    const double ipz = 1.0 / K.bin_p;
     double Px = 0.0, Py = 0.0;
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
         B.md[m] = make_float2(0.f, 0.f);
         if (m < K.nm) {
             const double2 md = *reinterpret_cast<const double2 *>(K.modes + (((size_t)m * K.nt + t) * K.nc + c) * 2);
-            B.md[m] = make_float2((float)md.x, (float)md.y);
+            // z = v / p directly: the modes and the mean carry 1/p (one
+            // rounding of md / p to f32, the same 2^-24 relative as md alone)
+            B.md[m] = make_float2((float)(md.x * ipz), (float)(md.y * ipz));
             const double w = cm[m];
             Px += fabs(md.x) * w;
             Py += fabs(md.y) * w;
         }
     }
-    B.mu = make_float2((float)mu.x, (float)mu.y);
+    B.mu = make_float2((float)(mu.x * ipz), (float)(mu.y * ipz));
     const double Tx = fabs(mu.x) + Px, Ty = fabs(mu.y) + Py;
     // |v32 - v64| <= delta (the k_vmax bound: f32 inputs, FMA chain, and the
-    // reference's own f64 rounding); then z = v32 * f32(1/p), floor/frac in
-    // f32: 2^-21 (|z| + 1) covers the scaling and the frac subtraction
+    // reference's own f64 rounding) -- here with the inputs pre-scaled by
+    // 1/p, |z32 - v64 / p| <= delta / p + 2^-24 |v| / p; then floor/frac in
+    // f32: 2^-21 (|z| + 1) covers that and the frac subtraction
     const double kRel = (2.0 * K.nm + 8.0) * 0x1p-24 * 1.001, kAbs = (K.nm + 2.0) * 0x1p-140;
     const double dlx = Tx * kRel + kAbs, dly = Ty * kRel + kAbs;
     const double ip = 1.0 / K.bin_p;
@@ -2151,7 +2155,6 @@ __device__ __forceinline__ int bin_loop(const BuildK &K, const BinCell *B, const
 {
     const int lane = threadIdx.x & 31, nr = K.nr;
     const int nch = K.nr_pad >> 5;   // a multiple of 4: coefficients zero-padded to 128-realization multiples
-    const float2 ip2 = make_float2(K.bin_ip, K.bin_ip);   // 1 / p (exactly 1 for p = 1)
     const float2 M2 = make_float2(12582912.0f, 12582912.0f);   // 1.5 * 2^23: floor by a round-down add
     const int ns = K.bin_ns;
     const float2 NS2 = make_float2((float)ns, (float)ns);
@@ -2232,7 +2235,7 @@ __device__ __forceinline__ int bin_loop(const BuildK &K, const BinCell *B, const
                     float2 v = B[q].mu;
 #pragma unroll
                     for (int m = 0; m < 8; ++m) v = ffma2_bcast(cf[m], B[q].md[m], v);
-                    const float2 z = f2_mul(v, ip2);
+                    const float2 z = v;   // the inputs carry 1/p (bin_setup)
                     const float2 t1 = f2_add_rm(z, M2);             // M + floor(z)
                     const float2 f = f2_sub(z, f2_sub(t1, M2));     // frac(z) in [0, 1] (z finite: F_PROVEN)
                     const float2 tb = f2_fma_rm(f, NS2, M2);        // M + floor(frac * NS), <= M + NS
@@ -2481,7 +2484,15 @@ __device__ __forceinline__ bool bin_task(const BuildK *__restrict__ Kg, unsigned
         int qn = 0;
         constexpr int RING = OB ? kBinRingO : kBinRing;
         // one loop instance (code size): a missing second cell never counts
-        if (ncl > 0) qn = bin_loop<2, OB, RING>(K, B, cid, two, t, tab_s, bins_s, ring_s, bq, drain_all);
+        // a lean pair with one live cell (|A| > 16: one cell per task) runs
+        // the one-cell instance -- half the reconstructions and counter
+        // updates of the pair loop, which would compute a dead second cell
+        if constexpr (!OB) {
+            if (ncl == 1) qn = bin_loop<1, OB, RING>(K, B, cid, false, t, tab_s, bins_s, ring_s, bq, drain_all);
+            else if (ncl > 1) qn = bin_loop<2, OB, RING>(K, B, cid, two, t, tab_s, bins_s, ring_s, bq, drain_all);
+        } else {
+            if (ncl > 0) qn = bin_loop<2, OB, RING>(K, B, cid, two, t, tab_s, bins_s, ring_s, bq, drain_all);
+        }
         if (qn < 0) return false;
         FM_STAT(5, lane == 0 ? 1 : 0);
 #ifdef FM_STATS
