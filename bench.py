@@ -428,14 +428,14 @@ def run_ours(args):
     fp32_peak = sm_count * 128 * 2 * f_clk
     cell_real = cells_rank * g.nt * w.n_realizations
     flops_cr = 4 * w.n_modes + 8
-    prof = _load_json(os.path.join(ROOT, "profiles", "r02_k_build_paper_ncu.json")) or {}
+    prof = _load_json(os.path.join(ROOT, "profiles", "r02d_k_build_paper_ncu.json")) or {}
     traffic = prof.get("dram_bytes_build") if args.workload == WORKLOAD else None
     issue = None
     if prof.get("warp_instructions_build") and args.workload == WORKLOAD and world == 1:
         ach_i = prof["warp_instructions_build"] / (kbuild_ms / 1e3)
         issue = {"achieved": ach_i / 1e12, "peak": sm_count * 4 * f_clk / 1e12, "unit": "Twarp-instr/s",
                  "frac": ach_i / (sm_count * 4 * f_clk),
-                 "note": "ncu executed warp instructions of one build (profiles/r02_k_build_paper_ncu.json) / "
+                 "note": "ncu executed warp instructions of one build (profiles/r02d_k_build_paper_ncu.json) / "
                          "this run's k_build time, against 4 issue slots per SM per clock"}
     fp64_ceiling = sm_count * 64 * f_clk
 
