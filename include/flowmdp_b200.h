@@ -300,6 +300,24 @@ int32_t fm_rollout(const fm_rollout_args *h_args, void *stream);
 int32_t fm_solve_backward(const fm_model *h_model, int32_t t_lo, int32_t t_hi,
                           double *values, uint16_t *policy, void *stream);
 
+/* Multi-GPU strip solve ("optional halo descriptors").  The
+ * model is one rank's y-strip (fm_model.cell0 / ncell, whole rows); its
+ * layers t = t_hi-1 .. t_lo are solved on `stream` as fm_solve_backward
+ * does, and after each layer -- V_t of the strip's rows enqueued -- `halo`
+ * is called with (user, t, stream) before layer t-1 is launched.  The hook
+ * enqueues the exchange of layer t's halo: it sends rows [j0, j0 + h_y) and
+ * [j1 - h_y, j1) of V_t and receives rows [j0 - h_y, j0) and [j1, j1 + h_y)
+ * into `values` (full-grid layout, state (t, j, i) at t*N_c + j*n_x + i),
+ * ordered with `stream` (e.g. ncclGroupStart; ncclSend / ncclRecv on the
+ * neighbours; ncclGroupEnd on `stream`, or peer copies / P2P stores), and
+ * returns 0; nonzero aborts with FM_BAD_ARG.  halo = NULL: no exchange (one
+ * rank).  Replaces the reference's per-slab fork pool (model_builder.py:
+ * 548-566) on the solve side; sharding.py's StripPlanner is the Python
+ * caller of the same scheme. */
+typedef int32_t (*fm_halo_fn)(void *user, int32_t t, void *stream);
+int32_t fm_solve_backward_halo(const fm_model *h_model, int32_t t_lo, int32_t t_hi, double *values,
+                               uint16_t *policy, fm_halo_fn halo, void *user, void *stream);
+
 /* One backward layer restricted to rows j in [j0, j1) (multi-GPU strips). */
 int32_t fm_solve_layer(const fm_model *h_model, int32_t t, int32_t j0, int32_t j1,
                        double *values, uint16_t *policy, void *stream);

@@ -119,6 +119,9 @@ class FmRolloutArgs(C.Structure):
 
 
 # exported symbols and their signatures; tests check every one resolves
+# fm_halo_fn: int32_t (*)(void *user, int32_t t, void *stream)
+HALO_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.c_void_p)
+
 SIGNATURES = {
     "fm_abi_version": (C.c_int32, []),
     "fm_last_error": (C.c_char_p, []),
@@ -145,6 +148,8 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "fm_solve_backward": (C.c_int32, [C.POINTER(FmModel), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                       C.c_void_p]),
+    "fm_solve_backward_halo": (C.c_int32, [C.POINTER(FmModel), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p]),
     "fm_solve_layer": (C.c_int32, [C.POINTER(FmModel), C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                    C.c_void_p, C.c_void_p]),
     "fm_prob_table": (C.c_int32, [C.c_int32, C.c_void_p, C.c_void_p]),

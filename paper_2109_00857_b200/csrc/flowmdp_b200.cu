@@ -3084,7 +3084,9 @@ __global__ void __launch_bounds__(128, PART == 3 ? FM_BUILD_MINB3
                     S = 0.0;
                     if (!(R.rflags & RF_DEAD)) {
                         const double *g_n = K.g + (size_t)(t + 1) * K.nc;
-                        for (int sl = 0; sl < nslot; ++sl) {
+                        // slots outside [s_lo, s_hi] hold no counts (a lean
+                        // binned row's range, see the emission below)
+                        for (int sl = s_lo; sl <= s_hi && sl < nslot; ++sl) {
                             const int cnt = h16[sl * 32];
                             if (!cnt) continue;
                             const int li = R.ci + sl % W - K.hx, lj = R.cj + sl / W - K.hy;
@@ -4396,6 +4398,30 @@ extern "C" int32_t fm_solve_backward(const fm_model *M, int32_t t_lo, int32_t t_
     for (int t = t_hi - 1; t >= t_lo; --t) {
         st = solve_layer(M, ptab, t, M->cell0 / M->nx, (M->cell0 + M->ncell) / M->nx, values, policy, s);
         if (st != FM_OK) return st;
+    }
+    FM_CK(cudaFreeAsync(ptab, s));
+    return FM_OK;
+}
+
+extern "C" int32_t fm_solve_backward_halo(const fm_model *M, int32_t t_lo, int32_t t_hi, double *values,
+                                          uint16_t *policy, fm_halo_fn halo, void *user, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    if (t_lo < 0 || t_hi > M->nt || t_lo >= t_hi) return fm_fail(FM_BAD_ARG, "fm_solve_backward_halo: bad t range");
+    if (M->ncell % M->nx || M->cell0 % M->nx)
+        return fm_fail(FM_BAD_ARG, "fm_solve_backward_halo: model strip not whole rows");
+    int32_t st;
+    double *ptab = prob_table(M, s, &st);
+    if (st != FM_OK) return st;
+    const int j0 = M->cell0 / M->nx, j1 = (M->cell0 + M->ncell) / M->nx;
+    for (int t = t_hi - 1; t >= t_lo; --t) {
+        st = solve_layer(M, ptab, t, j0, j1, values, policy, s);
+        if (st == FM_OK && halo && halo(user, t, stream) != 0)
+            st = fm_fail(FM_BAD_ARG, "fm_solve_backward_halo: halo hook failed at layer %d", t);
+        if (st != FM_OK) {
+            cudaFreeAsync(ptab, s);
+            return st;
+        }
     }
     FM_CK(cudaFreeAsync(ptab, s));
     return FM_OK;

@@ -553,7 +553,7 @@ def test_binned_build_equals_per_transition_build(case, monkeypatch):
 
 
 @pytest.mark.parametrize("case", ["smoke", "desk", "two_obstacles_1k"])
-def test_reward_sum_counts_net_energy(case):
+def test_reward_sum_counts_net_energy(case, monkeypatch):
     """reward_sum="counts" (fm_build_args.reward_mode 1): net-energy rows
     take the binned build; every COO block (rows, cols, f64 probabilities)
     stays bit-identical to the oracle's and every reward agrees with the
@@ -580,3 +580,8 @@ def test_reward_sum_counts_net_energy(case):
     assert rel.max() <= 1e-12
     seq = build_device_model(denv, acts, rcfg, target, sub).to_sparse_model()
     assert seq.rewards.tobytes() == om.rewards.tobytes()   # the default stays bit-exact
+    # the binned rows sum only their slot range; the per-transition path
+    # sums every slot -- same slot order, so the same bits
+    monkeypatch.setenv("FM_NO_BINS", "1")
+    pt = build_device_model(denv, acts, rcfg, target, sub, reward_sum="counts").to_sparse_model()
+    assert pt.rewards.tobytes() == sm.rewards.tobytes()

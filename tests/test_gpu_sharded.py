@@ -162,3 +162,69 @@ def test_strip_planner_pipelined(tmp_path, case, world, n_groups):
     assert res == 0.0
     assert got_v.tobytes() == ref_v.tobytes()
     assert np.array_equal(got_p, ref_a.astype(np.uint16))
+
+
+def _halo_case_desk():
+    env, acts, rcfg, target, _ = make_named_env("desk")
+    return env, acts, rcfg, target
+
+
+@pytest.mark.parametrize("nstrips", [2, 3])
+def test_solve_backward_halo_hook(nstrips):
+    """fm_solve_backward_halo (the C-ABI strip solve with a halo hook): per
+    strip, the hook fills layer t's halo rows -- here from a full-grid
+    solve, standing in for the neighbours' NCCL / P2P transfer -- before
+    layer t-1 runs; every strip's rows then equal the full solve bit for
+    bit, and a hook returning nonzero aborts with FM_BAD_ARG."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2109_00857_b200 import _lib
+    from paper_2109_00857_b200.builder import DeviceEnv, build_device_model
+    from paper_2109_00857_b200.sharding import strip_bounds
+    from paper_2109_00857_b200.solver import solve_backward
+    import paper_2109_00857_b200 as fm
+
+    env, acts, rcfg, target = _halo_case_desk()
+    g = env.grid
+    de = DeviceEnv.from_host(env)
+    sub = fm.compute_subgrid(env.field, acts, g, device_env=de)
+    full_v, full_p = solve_backward(build_device_model(de, acts, rcfg, target, sub))
+    hy = sub.half_width_y
+    L = _lib.load()
+    calls = []
+    for k in range(nstrips):
+        j0, j1 = strip_bounds(g.ny, nstrips, k)
+        dm = build_device_model(de, acts, rcfg, target, sub, j_range=(j0, j1))
+        m = dm.fm_model()
+        values = torch.zeros(g.n_states + 1, dtype=torch.float64, device="cuda")
+        policy = torch.zeros(g.n_states, dtype=torch.int16, device="cuda")
+
+        def hook(user, t, stream, j0=j0, j1=j1, values=values):
+            base = t * g.n_cells
+            for a, b in ((max(j0 - hy, 0), j0), (j1, min(j1 + hy, g.ny))):
+                if a < b:   # the neighbours' rows of V_t, enqueued on the solve stream
+                    values[base + a * g.nx:base + b * g.nx].copy_(full_v[base + a * g.nx:base + b * g.nx])
+            calls.append(t)
+            return 0
+
+        cb = _lib.HALO_FN(hook)
+        _lib.check(L.fm_solve_backward_halo(C.byref(m), 0, g.nt, values.data_ptr(), policy.data_ptr(),
+                                            C.cast(cb, C.c_void_p), None, _lib.stream_ptr()), "halo solve")
+        torch.cuda.synchronize()
+        for t in range(g.nt):
+            a, b = t * g.n_cells + j0 * g.nx, t * g.n_cells + j1 * g.nx
+            assert values[a:b].cpu().numpy().tobytes() == full_v[a:b].cpu().numpy().tobytes(), (k, t)
+            assert torch.equal(policy[a:b], full_p[a:b]), (k, t)
+    assert calls[:g.nt] == list(range(g.nt - 1, -1, -1))
+    # a failing hook aborts the sweep
+    bad = _lib.HALO_FN(lambda user, t, stream: 1)
+    j0, j1 = strip_bounds(g.ny, nstrips, 0)
+    dm = build_device_model(de, acts, rcfg, target, sub, j_range=(j0, j1))
+    m = dm.fm_model()
+    values = torch.zeros(g.n_states + 1, dtype=torch.float64, device="cuda")
+    policy = torch.zeros(g.n_states, dtype=torch.int16, device="cuda")
+    st = L.fm_solve_backward_halo(C.byref(m), 0, g.nt, values.data_ptr(), policy.data_ptr(),
+                                  C.cast(bad, C.c_void_p), None, _lib.stream_ptr())
+    assert st != 0
