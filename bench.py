@@ -60,6 +60,8 @@ def _args():
                         "per-slot counts (rewards within ~1e-13 relative; north_star tolerance 1e-5)")
     p.add_argument("--reserve-sms", type=int, default=2,
                    help="SMs the build leaves to the pipelined solve stream (with --groups > 1)")
+    p.add_argument("--upload-slabs", type=int, default=8,
+                   help="end-to-end path: time slabs of the host->device upload, each scanned as soon as it lands")
     p.add_argument("--group-ratio", type=float, default=0.6,
                    help="slab group k (launch order, highest t first) holds a share of the slabs proportional "
                         "to ratio**k: < 1 shrinks the groups toward t = 0, so less of the solve and of the "
@@ -354,7 +356,7 @@ def run_ours(args):
             e0.record()
             # upload in time slabs, the exact sub-grid scan of each slab
             # overlapping the next slab's copy (the planner's host-input path)
-            de = DeviceEnv.from_host_scanned(_HostEnv, j_range=(j0, j1) if world > 1 else None)
+            de = DeviceEnv.from_host_scanned(_HostEnv, slabs=args.upload_slabs, j_range=(j0, j1) if world > 1 else None)
             planner.denv = de
             dm = planner.step(scanned=True, sink=host_m, sink_stream=d2h_stream)
             stages.append(dict(planner.events, nnz=dm.nnz))
