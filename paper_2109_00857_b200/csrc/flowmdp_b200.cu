@@ -1012,7 +1012,7 @@ struct BuildK {
     int off_bring;                      // the coefficient ring (= off_bdense for lean tasks; separate for
                                         // obstacle tasks, which drain into the dense histogram mid-loop)
     const float *coef32;        // [t - t0][nr_pad][8] f32 coefficients (zero padded), per launch
-    int nr_pad;                 // realizations rounded up to a multiple of 128
+    int nr_pad;                 // realizations rounded up to whole bin-loop iterations (64 by default)
     const double *cmax;         // [t - t0][nm] max_r |coeff[t, r, m]|
     const int4 *envelope;       // [nt][nc] per-cell velocity envelope (fm_velocity_scan) or null
     int bin_ns;                 // buckets per unit of frac(z): the smallest of 32 / 64 / 128 giving the same zones
@@ -2154,7 +2154,7 @@ __device__ __forceinline__ int bin_loop(const BuildK &K, const BinCell *B, const
                                         Drain &&drain)
 {
     const int lane = threadIdx.x & 31, nr = K.nr;
-    const int nch = K.nr_pad >> 5;   // a multiple of 4: coefficients zero-padded to 128-realization multiples
+    const int nch = K.nr_pad >> 5;   // a multiple of H: coefficients zero-padded to whole iterations
     const float2 M2 = make_float2(12582912.0f, 12582912.0f);   // 1.5 * 2^23: floor by a round-down add
     const int ns = K.bin_ns;
     const float2 NS2 = make_float2((float)ns, (float)ns);
@@ -3989,7 +3989,10 @@ extern "C" int32_t fm_build_launch(const fm_build_args *h, fm_model *M, void *st
     double *cmax = nullptr;
     if (K.bin_ok) {
         const int nts = K.t1 - K.t0;
-        K.nr_pad = (K.nr + 127) & ~127;   // whole iterations of up to 4 chunks
+        // whole iterations of H chunks of 32 (H = 2, or FM_BIN_H with an
+        // 8-chunk ring): C2 pads 5000 -> 5056 realizations, not 5120
+        constexpr int kPadR = 32 * (FM_BIN_H > 2 ? FM_BIN_H : 2);
+        K.nr_pad = (K.nr + kPadR - 1) / kPadR * kPadR;
         FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&c32), sizeof(float) * 8 * (size_t)nts * K.nr_pad, s));
         FM_CK(cudaMallocAsync(reinterpret_cast<void **>(&cmax), sizeof(double) * (size_t)nts * (K.nm ? K.nm : 1), s));
         FM_CK(cudaMemsetAsync(cmax, 0, sizeof(double) * (size_t)nts * (K.nm ? K.nm : 1), s));
